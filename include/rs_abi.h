@@ -42,7 +42,7 @@ extern "C" {
 #define RS_MAX_BANDS 8     /* empirical-predictor prompt bands          */
 #define RS_NUM_TASKS 5     /* TaskKind, request.hpp:11-17               */
 #define RS_MAX_LAYERS 4    /* Q-network affine layers (dqn uses 3)      */
-#define RS_MAX_WIDTH 256   /* widest Q-network layer supported on device */
+#define RS_MAX_WIDTH 512   /* widest Q-network layer supported on device */
 
 typedef enum rs_status {
   RS_OK = 0,
@@ -90,7 +90,8 @@ typedef enum rs_replay_status {
   RS_REPLAY_NOT_ADMISSIBLE = 2,  /* logic_error, instance.hpp:209-211        */
   RS_REPLAY_BAD_ACTION = 3,      /* invalid_argument, env.hpp:252-254        */
   RS_REPLAY_CAPACITY = 4,        /* engine limit exceeded    */
-  RS_REPLAY_NOT_RUN = 5
+  RS_REPLAY_NOT_RUN = 5,
+  RS_REPLAY_INVALID_TRACE = 6    /* decreasing arrivals / tokens out of range */
 } rs_replay_status;
 
 /* HardwareProfile, latency.hpp:16-35 */
@@ -162,9 +163,6 @@ typedef struct rs_batch_cfg {
 } rs_batch_cfg;
 
 #define RS_FLAG_NONE 0u
-/* Skip the per-request output stores except completion (bench of the
- * compulsory traffic).  Not used by the parity tests. */
-#define RS_FLAG_STATS_ONLY 1u
 
 /* Struct-of-arrays trace batch, CSR over replays.  Request i of replay r is
  * element offsets[r] + i.  Field meaning follows Request (request.hpp:42-69). */
@@ -220,7 +218,9 @@ typedef struct rs_replay_stats {
   int32_t status;               /* rs_replay_status */
   int32_t error_instance;       /* instance that raised, or -1 */
   int32_t percentiles_valid;
-  int32_t _pad[7];
+  int32_t _pad0;
+  int64_t injected;             /* requests that reached the router queue */
+  int32_t _pad[4];
 } rs_replay_stats;
 
 /* ---- identity / device ------------------------------------------------ */
@@ -262,6 +262,10 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* trace,
                           rs_req_out* out, rs_replay_stats* stats,
                           void* workspace, size_t workspace_bytes,
                           void* cuda_stream);
+
+/* Pinned host memory for the _host entry points (cudaHostAlloc). */
+void* rs_host_alloc(size_t bytes);
+void rs_host_free(void* p);
 
 /* Host-buffer convenience: H2D, predictor, replay, stats, D2H on `device`.
  * This is the reference-facing call (evaluate_policy over seeds).  Any of the

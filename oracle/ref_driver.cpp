@@ -279,6 +279,7 @@ int run_one(const rs_batch_cfg& c, const ReplayIO& io, rs_replay_stats* st,
     if (io.preemptions) io.preemptions[i] = r.preemption_count;
     if (io.predicted) io.predicted[i] = static_cast<uint8_t>(r.predicted_bucket < 0 ? 255 : r.predicted_bucket);
     if (r.routed_time_s >= 0.0) st->routed += 1;
+    if (r.predicted_bucket >= 0) st->injected += 1;
     if (!r.completed()) continue;
     // compute_metrics order (metrics.hpp:94-121)
     st->total_e2e_s += r.completion_time_s - r.arrival_time_s;

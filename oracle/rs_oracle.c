@@ -674,6 +674,7 @@ int ora_run_replay(const rs_batch_cfg* c, int64_t n, const double* arrival,
     st->clock = S.clock;
     st->status = status;
     st->error_instance = S.error_instance;
+    st->injected = S.cursor;
     /* compute_metrics order, metrics.hpp:94-121 */
     double fa = DBL_MAX, lc = 0.0;
     double *e2e = (double*)malloc(nn * sizeof(double)), *ttft = (double*)malloc(nn * sizeof(double)),

@@ -21,7 +21,7 @@ RS_MAX_BUCKETS = 8
 RS_MAX_BANDS = 8
 RS_NUM_TASKS = 5
 RS_MAX_LAYERS = 4
-RS_MAX_WIDTH = 256
+RS_MAX_WIDTH = 512
 
 # rs_status
 RS_OK = 0
@@ -55,6 +55,7 @@ REPLAY_NOT_ADMISSIBLE = 2
 REPLAY_BAD_ACTION = 3
 REPLAY_CAPACITY = 4
 REPLAY_NOT_RUN = 5
+REPLAY_INVALID_TRACE = 6
 
 # Table 1 predictor accuracies (workload.hpp:165-174), TaskKind order.
 DATASET_ACCURACY = (0.9310, 0.7036, 0.7992, 0.6527, 0.9506)
@@ -165,7 +166,9 @@ class ReplayStats(C.Structure):
         ("status", C.c_int32),
         ("error_instance", C.c_int32),
         ("percentiles_valid", C.c_int32),
-        ("_pad", C.c_int32 * 7),
+        ("_pad0", C.c_int32),
+        ("injected", C.c_int64),
+        ("_pad", C.c_int32 * 4),
     ]
 
 
@@ -183,7 +186,7 @@ STATS_DTYPE = np.dtype(
                                  "e2e_p99", "ttft_p50", "ttft_p90", "ttft_p99", "tbt_p50",
                                  "tbt_p90", "tbt_p99")]
     + [("status", np.int32), ("error_instance", np.int32), ("percentiles_valid", np.int32),
-       ("_pad", np.int32, (7,))])
+       ("_pad0", np.int32), ("injected", np.int64), ("_pad", np.int32, (4,))])
 assert STATS_DTYPE.itemsize == 256
 
 
@@ -279,7 +282,7 @@ EXPORTED_SYMBOLS = (
     "rs_validate_config", "rs_workspace_size", "rs_predict_buckets",
     "rs_replay_batch", "rs_replay_batch_host", "rs_mlp_forward_host",
     "rs_generate_mixture", "rs_generate_mixture_batch", "rs_mix_seed",
-    "rs_heavy_decode_cutoff",
+    "rs_heavy_decode_cutoff", "rs_host_alloc", "rs_host_free",
 )
 
 
@@ -309,6 +312,9 @@ def _declare(lib: C.CDLL) -> None:
     lib.rs_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
     lib.rs_heavy_decode_cutoff.restype = C.c_int64
     lib.rs_heavy_decode_cutoff.argtypes = [P(Profile), P(Thresholds)]
+    lib.rs_host_alloc.restype = C.c_void_p
+    lib.rs_host_alloc.argtypes = [C.c_size_t]
+    lib.rs_host_free.argtypes = [C.c_void_p]
 
 
 def last_error(lib: C.CDLL) -> str:

@@ -1,0 +1,261 @@
+// common.cuh — device-side shared definitions of the B200 replay engine.
+//
+// Numerics: every fp64 operation that the reference performs is issued here
+// as an explicitly rounded __dadd_rn / __dmul_rn / __ddiv_rn in the
+// reference's evaluation order, and the library is compiled with
+// -fmad=false, so no DFMA contraction can change a clock.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rs_abi.h"
+
+namespace rs {
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kMaxRunChunks = 4;                 // running entries per lane
+constexpr int kMaxRunCap = kMaxRunChunks * kWarp;  // 128 running per instance
+constexpr int kMaxInstances = 128;
+constexpr int kMaxFront = 32;                    // min_min stuck-front list
+constexpr uint32_t kNil = 0xffffffffu;
+
+// Per-instance scalar block kept in shared memory (the router snapshot
+// aggregates are maintained here so a tick never rescans a queue).
+struct __align__(16) InstHot {
+  double clock;           // Instance::clock_
+  long long res_wait;     // sum reserved_tokens over waiting
+  long long pend_wait;    // sum prompt over waiting
+  long long dleft_wait;   // sum decode_left over waiting
+  long long tleft_wait;   // sum max(0, true - emitted) over waiting
+  long long tok_wait;     // sum prompt + emitted over waiting (token mass)
+  int n_run;              // running_.size()
+  int n_prefill;          // running entries with prompt_remaining > 0
+  int res_run;            // sum reserved_tokens over running
+  int kv_run;             // kv_tokens_in_use (sum footprint)
+  int pend_run;           // sum prompt_remaining over running
+  int dleft_run;          // sum decode_left over running
+  int tleft_run;          // sum true - emitted over running
+  int tok_run;            // sum prompt + emitted over running
+  int min_dleft;          // min decode_left over running (INT_MAX if none)
+  int w_head, w_cnt;      // shared-memory waiting ring
+  int o_cnt;              // overflow (global doubly linked list)
+  int o_head, o_tail;
+  int _pad0, _pad1;
+};
+static_assert(sizeof(InstHot) == 112, "InstHot layout");
+
+// Launch parameters (kernel argument block, read through the constant bank).
+struct KParams {
+  // HardwareProfile (latency.hpp:16-35)
+  double tpp, intercept, dpt, dtb;
+  double delta_t;
+  // ImpactConfig (impact.hpp:14-32)
+  double grad1, grad2, eps_s, alpha;
+  double rl_eps;
+  double accuracy[RS_NUM_TASKS];
+  int prompt_exp;
+  int kv_cap;
+  int max_batch;
+  int batching;
+  int chunk;
+  int m;
+  int n_state_edges;
+  int n_pred_edges;
+  int state_edges[RS_MAX_BUCKETS];
+  int pred_edges[RS_MAX_BUCKETS];
+  int ub[RS_MAX_BUCKETS];          // upper_bound_tokens per predicted bucket
+  int n_band_edges;
+  int band_edges[RS_MAX_BANDS];
+  uint8_t emp_table[RS_NUM_TASKS][RS_MAX_BANDS];
+  int predictor_mode;
+  int rcap, wcap;                  // running / waiting-ring capacity
+  int dsl_cutoff;
+  unsigned flags;
+  long long max_ticks;
+  // Q-network (transposed layout in workspace, see replay.cu)
+  int rl_layers;
+  int rl_dims[RS_MAX_LAYERS + 1];
+  int rl_woff[RS_MAX_LAYERS];      // offset of W^T of layer l (doubles)
+  int rl_boff[RS_MAX_LAYERS];      // offset of b of layer l
+  const double* rl_w;               // reference flat layout (device)
+  int rl_maxw;                     // widest hidden layer
+  int smem_weights_bytes;          // staged W^T + b at the start of smem
+  // trace (CSR over replays)
+  int num_replays;
+  const long long* offsets;
+  const double* arrival;
+  const int* prompt;
+  const int* decode;
+  const uint8_t* task;
+  const uint8_t* bucket;           // predicted buckets (rs_predict_buckets)
+  const uint64_t* policy_seed;
+  // outputs
+  int* o_instance;
+  double* o_routed;
+  double* o_first;
+  double* o_completion;
+  int* o_preempt;
+  uint8_t* o_pred;
+  rs_replay_stats* stats;
+  // workspace
+  uint32_t* ov_next;
+  uint32_t* ov_prev;
+  int* ov_emit;
+  uint8_t* mm_removed;
+  int* work_counter;
+  // shared-memory layout (bytes, per replay group)
+  int smem_group_bytes;
+  int off_run, off_wait, off_dbc, off_rlx, off_rng, off_front;
+};
+
+// ---------------------------------------------------------------- helpers
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & (kWarp - 1); }
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ int warp_sum(int v) {
+  return (int)__reduce_add_sync(kFull, (unsigned)v);
+}
+__device__ __forceinline__ int warp_min(int v) { return __reduce_min_sync(kFull, v); }
+__device__ __forceinline__ int warp_max(int v) { return __reduce_max_sync(kFull, v); }
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(kFull, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long w = __shfl_xor_sync(kFull, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Inclusive prefix sum across the warp.
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int l = lane_id();
+#pragma unroll
+  for (int o = 1; o < kWarp; o <<= 1) {
+    int t = __shfl_up_sync(kFull, v, o);
+    if (l >= o) v += t;
+  }
+  return v;
+}
+
+// Total order on doubles matching operator< for non-NaN values, with -0
+// folded onto +0 (the reference compares with < / >, where they are equal).
+__device__ __forceinline__ unsigned long long ordered_key(double x) {
+  if (x == 0.0) x = 0.0;
+  unsigned long long u = (unsigned long long)__double_as_longlong(x);
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// Lowest lane index whose value is minimal among `valid` lanes; -1 if none.
+__device__ __forceinline__ int warp_argmin_key(unsigned long long key, bool valid) {
+  unsigned long long k = valid ? key : ~0ull;
+  unsigned long long mn = warp_min_u64(k);
+  unsigned ok = __ballot_sync(kFull, valid && k == mn);
+  return ok ? __ffs(ok) - 1 : -1;
+}
+__device__ __forceinline__ int warp_argmax_key(unsigned long long key, bool valid) {
+  unsigned long long k = valid ? key : 0ull;
+  unsigned long long mx = warp_max_u64(k);
+  unsigned ok = __ballot_sync(kFull, valid && k == mx);
+  return ok ? __ffs(ok) - 1 : -1;
+}
+
+// BucketScheme::bucket_of (predictor.hpp:34-40)
+__device__ __forceinline__ int bucket_of(const int* edges, int n, long long tokens) {
+  int b = 0;
+  for (int i = 1; i < n; ++i)
+    if (tokens >= edges[i]) b = i;
+  return b;
+}
+
+// mix of a decision into the per-replay FNV-1a hash (same as the oracles)
+__device__ __forceinline__ unsigned long long hash_action(unsigned long long h, int a) {
+  return (h ^ (unsigned long long)(unsigned)(a + 1)) * 0x100000001b3ull;
+}
+
+// ----------------------------------------------------- std::mt19937_64
+// Warp-cooperative block generation of 312 outputs into shared memory.
+// `s` holds the 312-word state.  Three dependency phases of the twist
+// (i < 156 reads only old words; 156 <= i < 311 reads new s[i-156]; i = 311
+// reads new s[0]), then tempering.
+__device__ inline void mt_twist_warp(unsigned long long* s) {
+  const int l = lane_id();
+  auto tw = [](unsigned long long a, unsigned long long b) {
+    unsigned long long x = (a & 0xFFFFFFFF80000000ull) | (b & 0x7FFFFFFFull);
+    unsigned long long xa = x >> 1;
+    if (x & 1ull) xa ^= 0xB5026F5AA96619E9ull;
+    return xa;
+  };
+  unsigned long long nv[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    int i = l + 32 * k;
+    if (i < 156) nv[k] = s[i + 156] ^ tw(s[i], s[i + 1]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    int i = l + 32 * k;
+    if (i < 156) s[i] = nv[k];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    int i = 156 + l + 32 * k;
+    if (i < 311) nv[k] = s[i - 156] ^ tw(s[i], s[i + 1]);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    int i = 156 + l + 32 * k;
+    if (i < 311) s[i] = nv[k];
+  }
+  __syncwarp();
+  if (l == 0) s[311] = s[155] ^ tw(s[311], s[0]);
+  __syncwarp();
+}
+
+__device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
+  y ^= (y >> 29) & 0x5555555555555555ull;
+  y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+  y ^= (y << 37) & 0xFFF7EEE000000000ull;
+  y ^= y >> 43;
+  return y;
+}
+
+// Seeding (std::mt19937_64 constructor); serial recurrence, lane 0.
+__device__ inline void mt_seed_warp(unsigned long long* s, unsigned long long seed) {
+  if (lane_id() == 0) {
+    s[0] = seed;
+    for (int i = 1; i < 312; ++i)
+      s[i] = 6364136223846793005ull * (s[i - 1] ^ (s[i - 1] >> 62)) + (unsigned long long)i;
+  }
+  __syncwarp();
+}
+
+// Rng::uniform (rng.hpp:29): (u64 >> 11) * 2^-53, exact.
+__device__ __forceinline__ double u01(unsigned long long v) {
+  return __dmul_rn((double)(v >> 11), 0x1.0p-53);
+}
+
+}  // namespace rs

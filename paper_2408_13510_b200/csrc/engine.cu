@@ -1,0 +1,509 @@
+// engine.cu — host side of the C ABI (include/rs_abi.h): configuration
+// validation, workspace layout, launch sizing and the device / host entry
+// points.  All compute happens in the sm_100a kernels of predictor.cuh,
+// replay.cuh, router.cuh and mlp.cuh; there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rs_abi.h"
+#include "common.cuh"
+#include "mlp.cuh"
+#include "predictor.cuh"
+#include "router.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+rs_status fail(rs_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define RS_CUDA(call)                                                             \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess) {                                                      \
+      return fail(e_ == cudaErrorMemoryAllocation ? RS_ERR_OUT_OF_MEMORY          \
+                                                  : RS_ERR_CUDA,                  \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));            \
+    }                                                                             \
+  } while (0)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// upper_bound_tokens (predictor.hpp:44-51) for every predicted bucket.
+int64_t ub_of(const rs_batch_cfg& c, int b) {
+  return b + 1 < c.n_predictor_edges ? c.predictor_edges[b + 1] : c.predictor_top_cap;
+}
+
+bool device_ok(int dev) {
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return false;
+  return p.major == 10;  // sm_100 family (the library carries sm_100a code)
+}
+
+rs_status require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail(RS_ERR_NO_DEVICE, "no CUDA device (the engine has no CPU fallback)");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!device_ok(dev)) return fail(RS_ERR_NO_DEVICE, "current device is not sm_100");
+  return RS_OK;
+}
+
+// Smem layout of one replay group (one warp) for this config.
+struct Layout {
+  int rcap, wcap;
+  int off_run, off_wait, off_dbc, off_rlx, off_rng, off_front, group_bytes;
+  int weights_bytes;
+  int woff[RS_MAX_LAYERS], boff[RS_MAX_LAYERS];
+  int maxw;
+};
+
+int min_reservation(const rs_batch_cfg& c) {
+  int64_t mn = c.predictor_top_cap;
+  for (int b = 0; b < c.n_predictor_edges; ++b) mn = std::min<int64_t>(mn, ub_of(c, b));
+  return (int)std::max<int64_t>(2, 1 + mn);
+}
+
+Layout make_layout(const rs_batch_cfg& c, int wcap) {
+  Layout L{};
+  const int m = c.num_instances;
+  L.rcap = (int)std::min<int64_t>(c.max_batch_size, c.kv_capacity_tokens / min_reservation(c));
+  if (L.rcap < 1) L.rcap = 1;
+  L.wcap = wcap;
+  size_t off = (size_t)m * sizeof(rs::InstHot);
+  L.off_run = (int)off;
+  off = align_up(off + 6ull * m * L.rcap * sizeof(int), 16);
+  L.off_wait = (int)off;
+  off = align_up(off + 5ull * m * L.wcap * sizeof(int), 16);
+  L.off_dbc = (int)off;
+  const bool rl = c.policy == RS_POLICY_RL;
+  if (rl) off = align_up(off + (size_t)m * RS_MAX_BUCKETS * sizeof(int), 16);
+  L.off_rlx = (int)off;
+  L.maxw = 0;
+  if (rl) {
+    for (int l = 1; l < c.rl_num_layers; ++l) L.maxw = std::max(L.maxw, c.rl_dims[l]);
+    L.maxw = std::max(L.maxw, 1);
+    off = align_up(off + (size_t)(c.rl_dims[0] + 2 * L.maxw) * sizeof(double), 16);
+  }
+  L.off_rng = (int)off;
+  if (rl && c.rl_epsilon > 0.0) off = align_up(off + 624 * sizeof(unsigned long long), 16);
+  L.off_front = (int)off;
+  if (c.policy == RS_POLICY_MIN_MIN) off = align_up(off + rs::kMaxFront * sizeof(int), 16);
+  L.group_bytes = (int)align_up(off, 128);
+  L.weights_bytes = 0;
+  if (rl) {
+    size_t w = 0;
+    for (int l = 0; l < c.rl_num_layers; ++l) {
+      L.woff[l] = (int)w;
+      w += (size_t)c.rl_dims[l] * c.rl_dims[l + 1];
+      L.boff[l] = (int)w;
+      w += (size_t)c.rl_dims[l + 1];
+    }
+    L.weights_bytes = (int)align_up(w * sizeof(double), 128);
+  }
+  return L;
+}
+
+rs_status validate(const rs_batch_cfg* c) {
+  if (!c) return fail(RS_ERR_INVALID_ARGUMENT, "null config");
+  if (c->abi_version != RS_ABI_VERSION) return fail(RS_ERR_INVALID_ARGUMENT, "abi_version mismatch");
+  const rs_profile& p = c->profile;  // HardwareProfile::validate, latency.hpp:25-34
+  if (!(p.prompt_time_per_token > 0.0) || !(p.prompt_time_intercept > 0.0) ||
+      !(p.decode_time_per_token > 0.0) || !(p.decode_time_base > 0.0))
+    return fail(RS_ERR_INVALID_ARGUMENT, "profile: all fields must be > 0");
+  if (p.prompt_time_per_token <= p.decode_time_per_token)
+    return fail(RS_ERR_INVALID_ARGUMENT,
+                "profile: prompt_time_per_token must exceed decode_time_per_token");
+  const rs_thresholds& t = c->thresholds;  // latency.hpp:42-50
+  if (!(t.heavy_prompt_seconds > 0.0) || !(t.heavy_decode_seconds > 0.0))
+    return fail(RS_ERR_INVALID_ARGUMENT, "thresholds: values must be > 0");
+  if (t.heavy_decode_seconds <= t.heavy_prompt_seconds)
+    return fail(RS_ERR_INVALID_ARGUMENT,
+                "thresholds: heavy_decode_seconds must exceed heavy_prompt_seconds");
+  const rs_impact& im = c->impact;  // impact.hpp:21-31
+  if (!(im.grad1 > 0.0) || !(im.grad2 > 0.0) || !(im.epsilon_s > 0.0))
+    return fail(RS_ERR_INVALID_ARGUMENT, "impact: grad1, grad2, epsilon_s must be > 0");
+  if (im.alpha < 0.0 || im.alpha > 1.0) return fail(RS_ERR_INVALID_ARGUMENT, "impact: alpha outside [0, 1]");
+  if (im.prompt_exponent != 1 && im.prompt_exponent != 2)
+    return fail(RS_ERR_INVALID_ARGUMENT, "impact: prompt_exponent must be 1 or 2");
+  if (c->kv_capacity_tokens < 1) return fail(RS_ERR_INVALID_ARGUMENT, "kv_capacity_tokens must be >= 1");
+  if (c->max_batch_size < 1) return fail(RS_ERR_INVALID_ARGUMENT, "max_batch_size must be >= 1");
+  if (c->chunk_size < 0) return fail(RS_ERR_INVALID_ARGUMENT, "chunk_size must be >= 1 (or 0 = off)");
+  if (c->batching < 0 || c->batching > 2) return fail(RS_ERR_INVALID_ARGUMENT, "unknown batching policy");
+  if (c->num_instances < 1) return fail(RS_ERR_INVALID_ARGUMENT, "cluster: num_instances must be >= 1");
+  if (!(c->delta_t > 0.0)) return fail(RS_ERR_INVALID_ARGUMENT, "cluster: delta_t must be > 0");
+  if (c->policy < 0 || c->policy >= RS_POLICY_COUNT) return fail(RS_ERR_INVALID_ARGUMENT, "unknown routing policy");
+  auto check_edges = [](const int64_t* e, int n, const char* what) -> rs_status {
+    if (n < 1 || n > RS_MAX_BUCKETS) return fail(RS_ERR_UNSUPPORTED, std::string(what) + ": 1..8 edges supported");
+    if (e[0] != 0) return fail(RS_ERR_INVALID_ARGUMENT, std::string(what) + ": first edge must be 0");
+    for (int i = 1; i < n; ++i)
+      if (e[i] <= e[i - 1]) return fail(RS_ERR_INVALID_ARGUMENT, std::string(what) + ": edges must ascend");
+    if (e[n - 1] > rs::kMaxTokens) return fail(RS_ERR_UNSUPPORTED, std::string(what) + ": edge above 2^20");
+    return RS_OK;
+  };
+  rs_status s;
+  if ((s = check_edges(c->predictor_edges, c->n_predictor_edges, "predictor scheme")) != RS_OK) return s;
+  if ((s = check_edges(c->state_edges, c->n_state_edges, "state scheme")) != RS_OK) return s;
+  if (c->predictor_top_cap < 1 || c->predictor_top_cap > rs::kMaxTokens)
+    return fail(RS_ERR_UNSUPPORTED, "predictor_top_cap outside [1, 2^20]");
+  for (int k = 0; k < RS_NUM_TASKS; ++k)
+    if (c->accuracy[k] < 0.0 || c->accuracy[k] > 1.0)
+      return fail(RS_ERR_INVALID_ARGUMENT, "accuracy outside [0,1]");
+  if (c->predictor_mode < 0 || c->predictor_mode > 2) return fail(RS_ERR_INVALID_ARGUMENT, "unknown predictor mode");
+  if (c->predictor_mode == RS_PREDICTOR_EMPIRICAL) {
+    if ((s = check_edges(c->band_edges, c->n_band_edges, "band scheme")) != RS_OK) return s;
+    for (int t2 = 0; t2 < RS_NUM_TASKS; ++t2)
+      for (int b = 0; b < c->n_band_edges; ++b)
+        if (c->empirical_table[t2][b] >= c->n_predictor_edges)
+          return fail(RS_ERR_INVALID_ARGUMENT, "empirical_table bucket out of range");
+  }
+  // engine limits: 32-bit token arithmetic on device
+  if (c->kv_capacity_tokens > (1ll << 30)) return fail(RS_ERR_UNSUPPORTED, "kv_capacity_tokens above 2^30");
+  if (c->num_instances > rs::kMaxInstances) return fail(RS_ERR_UNSUPPORTED, "more than 128 instances");
+  const int rcap = (int)std::min<int64_t>(c->max_batch_size, c->kv_capacity_tokens / min_reservation(*c));
+  if (rcap > rs::kMaxRunCap) return fail(RS_ERR_UNSUPPORTED, "more than 128 concurrently running requests per instance");
+  if (c->policy == RS_POLICY_RL) {
+    if (c->rl_num_layers < 1 || c->rl_num_layers > RS_MAX_LAYERS)
+      return fail(RS_ERR_INVALID_ARGUMENT, "rl: 1..4 layers");
+    for (int l = 0; l <= c->rl_num_layers; ++l)
+      if (c->rl_dims[l] < 1 || c->rl_dims[l] > RS_MAX_WIDTH)
+        return fail(RS_ERR_UNSUPPORTED, "rl: layer width outside [1, 512]");
+    if (c->rl_dims[0] != c->num_instances * (3 + c->n_state_edges) + 3)
+      return fail(RS_ERR_INVALID_ARGUMENT, "rl: input width != state_dimension (env.hpp:78-80)");
+    if (c->rl_dims[c->rl_num_layers] != c->num_instances + 1)
+      return fail(RS_ERR_INVALID_ARGUMENT, "rl: output width != num_instances + 1");
+    if (!c->rl_params) return fail(RS_ERR_INVALID_ARGUMENT, "rl: null parameters");
+    if (c->rl_epsilon < 0.0 || c->rl_epsilon > 1.0) return fail(RS_ERR_INVALID_ARGUMENT, "rl: epsilon outside [0,1]");
+  }
+  if (c->max_ticks < 0) return fail(RS_ERR_INVALID_ARGUMENT, "max_ticks must be >= 0");
+  return RS_OK;
+}
+
+// heavy_decode_token_cutoff (latency.hpp:132-138)
+int64_t heavy_cutoff(const rs_profile& p, const rs_thresholds& t) {
+  int64_t c = (int64_t)std::ceil(t.heavy_decode_seconds / p.decode_time_base - 1e-12);
+  while (!(p.decode_time_base * (double)c >= t.heavy_decode_seconds)) ++c;
+  return c;
+}
+
+struct WsLayout {
+  size_t counter, next, prev, emit, removed, total;
+};
+WsLayout ws_layout(int64_t total_requests) {
+  WsLayout w;
+  size_t off = 0;
+  w.counter = off;
+  off = align_up(off + 256, 256);
+  w.next = off;
+  off = align_up(off + 4ull * total_requests, 256);
+  w.prev = off;
+  off = align_up(off + 4ull * total_requests, 256);
+  w.emit = off;
+  off = align_up(off + 4ull * total_requests, 256);
+  w.removed = off;
+  off = align_up(off + (size_t)total_requests, 256);
+  w.total = off;
+  return w;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+template <int POL>
+rs_status launch_replay(const rs::KParams& kp, int wpb, int block_smem, int num_replays,
+                        cudaStream_t st) {
+  auto kern = rs::replay_kernel<POL>;
+  RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, block_smem));
+  int dev = 0, sms = 0, per_sm = 0;
+  RS_CUDA(cudaGetDevice(&dev));
+  RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * rs::kWarp, block_smem));
+  if (per_sm < 1) return fail(RS_ERR_UNSUPPORTED, "replay kernel does not fit on an SM");
+  const int want = (num_replays + wpb - 1) / wpb;
+  const int grid = std::max(1, std::min(want, sms * per_sm));
+  kern<<<grid, wpb * rs::kWarp, block_smem, st>>>(kp);
+  RS_CUDA(cudaGetLastError());
+  return RS_OK;
+}
+
+}  // namespace
+
+namespace rs {
+void set_error(const std::string& m) { g_err = m; }
+}  // namespace rs
+
+extern "C" {
+
+uint32_t rs_abi_version(void) { return RS_ABI_VERSION; }
+
+int32_t rs_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int ok = 0;
+  for (int d = 0; d < n; ++d) ok += device_ok(d) ? 1 : 0;
+  return ok;
+}
+
+rs_status rs_last_error(char* buf, size_t len) {
+  if (!buf || len == 0) return RS_ERR_INVALID_ARGUMENT;
+  std::snprintf(buf, len, "%s", g_err.c_str());
+  return RS_OK;
+}
+
+uint64_t rs_mix_seed(uint64_t seed, uint64_t stream) {  // rng.hpp:11-16
+  uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (stream + 1);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+int64_t rs_heavy_decode_cutoff(const rs_profile* p, const rs_thresholds* t) {
+  if (!p || !t) return -1;
+  return heavy_cutoff(*p, *t);
+}
+
+rs_status rs_default_config(rs_batch_cfg* c) {
+  if (!c) return fail(RS_ERR_INVALID_ARGUMENT, "null config");
+  std::memset(c, 0, sizeof(*c));
+  c->abi_version = RS_ABI_VERSION;
+  c->policy = RS_POLICY_ROUND_ROBIN;
+  c->profile = rs_profile{3.2e-4, 0.026, 3.3e-5, 0.0167};   // latency.hpp:17-20
+  c->thresholds = rs_thresholds{0.5, 5.0};                  // latency.hpp:39-40
+  c->impact = rs_impact{3.2e-4, 3.3e-5, 0.5, 0.5, 2, 0};    // impact.hpp:15-19
+  c->kv_capacity_tokens = 16384;                            // instance.hpp:38-41
+  c->max_batch_size = 128;
+  c->batching = RS_BATCHING_FCFS;
+  c->chunk_size = 0;
+  c->num_instances = 4;                                     // experiment.hpp:52-53
+  c->delta_t = 0.02;
+  c->n_predictor_edges = 4;                                 // predictor.hpp:55
+  const int64_t pe[4] = {0, 250, 1000, 4000};
+  std::memcpy(c->predictor_edges, pe, sizeof(pe));
+  c->n_state_edges = 3;                                     // predictor.hpp:59
+  const int64_t se[3] = {0, 256, 2048};
+  std::memcpy(c->state_edges, se, sizeof(se));
+  c->predictor_top_cap = 4096;                              // workload.hpp:23
+  c->predictor_mode = RS_PREDICTOR_SIMULATED;
+  const double acc[5] = {0.9310, 0.7036, 0.7992, 0.6527, 0.9506};  // workload.hpp:165-174
+  std::memcpy(c->accuracy, acc, sizeof(acc));
+  c->n_band_edges = 7;                                      // predictor.hpp:162-164
+  const int64_t be[7] = {0, 32, 64, 128, 256, 512, 1024};
+  std::memcpy(c->band_edges, be, sizeof(be));
+  c->max_ticks = 10000000;                                  // env.hpp:326
+  return RS_OK;
+}
+
+rs_status rs_validate_config(const rs_batch_cfg* cfg) { return validate(cfg); }
+
+rs_status rs_workspace_size(const rs_batch_cfg* cfg, int32_t num_replays,
+                            int64_t total_requests, size_t* bytes) {
+  rs_status s = validate(cfg);
+  if (s != RS_OK) return s;
+  if (!bytes || num_replays < 0 || total_requests < 0)
+    return fail(RS_ERR_INVALID_ARGUMENT, "bad workspace query");
+  *bytes = ws_layout(total_requests).total;
+  return RS_OK;
+}
+
+void* rs_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    g_err = "cudaHostAlloc failed";
+    return nullptr;
+  }
+  return p;
+}
+
+void rs_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+rs_status rs_predict_buckets(const rs_batch_cfg* cfg, const rs_trace_soa* tr,
+                             uint8_t* predicted_bucket, void* stream) {
+  rs_status s = validate(cfg);
+  if (s != RS_OK) return s;
+  if ((s = require_device()) != RS_OK) return s;
+  if (!tr || !predicted_bucket) return fail(RS_ERR_INVALID_ARGUMENT, "null trace/output");
+  if (tr->num_replays == 0) return RS_OK;
+  if (cfg->predictor_mode == RS_PREDICTOR_GIVEN && !tr->given_bucket)
+    return fail(RS_ERR_INVALID_ARGUMENT, "GIVEN predictor mode needs trace->given_bucket");
+  if (cfg->predictor_mode == RS_PREDICTOR_SIMULATED && !tr->predictor_seed)
+    return fail(RS_ERR_INVALID_ARGUMENT, "simulated predictor needs trace->predictor_seed");
+  rs::PredParams pp;
+  std::memset(&pp, 0, sizeof(pp));
+  std::memcpy(pp.accuracy, cfg->accuracy, sizeof(pp.accuracy));
+  pp.n_pred_edges = cfg->n_predictor_edges;
+  for (int i = 0; i < cfg->n_predictor_edges; ++i) pp.pred_edges[i] = (int)cfg->predictor_edges[i];
+  pp.n_band_edges = cfg->n_band_edges;
+  for (int i = 0; i < cfg->n_band_edges && i < RS_MAX_BANDS; ++i) pp.band_edges[i] = (int)cfg->band_edges[i];
+  std::memcpy(pp.emp_table, cfg->empirical_table, sizeof(pp.emp_table));
+  pp.mode = cfg->predictor_mode;
+  pp.num_replays = tr->num_replays;
+  pp.offsets = reinterpret_cast<const long long*>(tr->offsets);
+  pp.prompt = tr->prompt_tokens;
+  pp.decode = tr->decode_tokens;
+  pp.task = tr->task;
+  pp.given = tr->given_bucket;
+  pp.seeds = tr->predictor_seed;
+  pp.out = predicted_bucket;
+  int dev = 0, sms = 0;
+  RS_CUDA(cudaGetDevice(&dev));
+  RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int blocks_needed = (tr->num_replays + rs::kPredWarpsPerBlock - 1) / rs::kPredWarpsPerBlock;
+  const int grid = std::max(1, std::min(blocks_needed, sms * 8));
+  rs::predict_kernel<<<grid, rs::kWarp * rs::kPredWarpsPerBlock, 0, (cudaStream_t)stream>>>(pp);
+  RS_CUDA(cudaGetLastError());
+  return RS_OK;
+}
+
+rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_out* out,
+                          rs_replay_stats* stats, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  rs_status s = validate(cfg);
+  if (s != RS_OK) return s;
+  if ((s = require_device()) != RS_OK) return s;
+  if (!tr || !out || !stats) return fail(RS_ERR_INVALID_ARGUMENT, "null trace/out/stats");
+  if (tr->num_replays < 0) return fail(RS_ERR_INVALID_ARGUMENT, "num_replays < 0");
+  if (tr->num_replays == 0) return RS_OK;
+  if (!out->instance || !out->routed_s || !out->first_token_s || !out->completion_s ||
+      !out->preemptions || !out->predicted_bucket)
+    return fail(RS_ERR_INVALID_ARGUMENT, "rs_replay_batch needs every per-request output array");
+  if (cfg->policy == RS_POLICY_RL && cfg->rl_epsilon > 0.0 && !tr->policy_seed)
+    return fail(RS_ERR_INVALID_ARGUMENT, "epsilon-greedy needs trace->policy_seed");
+  const WsLayout wl = ws_layout(tr->total_requests);
+  if (!workspace || workspace_bytes < wl.total)
+    return fail(RS_ERR_INVALID_ARGUMENT, "workspace too small (rs_workspace_size)");
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = static_cast<char*>(workspace);
+
+  const int wcap = std::max(8, std::min(128, env_int("RS_WAIT_RING", 64)));
+  Layout L = make_layout(*cfg, wcap);
+  rs::KParams kp;
+  std::memset(&kp, 0, sizeof(kp));
+  const rs_profile& p = cfg->profile;
+  kp.tpp = p.prompt_time_per_token;
+  kp.intercept = p.prompt_time_intercept;
+  kp.dpt = p.decode_time_per_token;
+  kp.dtb = p.decode_time_base;
+  kp.delta_t = cfg->delta_t;
+  kp.grad1 = cfg->impact.grad1;
+  kp.grad2 = cfg->impact.grad2;
+  kp.eps_s = cfg->impact.epsilon_s;
+  kp.alpha = cfg->impact.alpha;
+  kp.rl_eps = cfg->rl_epsilon;
+  std::memcpy(kp.accuracy, cfg->accuracy, sizeof(kp.accuracy));
+  kp.prompt_exp = cfg->impact.prompt_exponent;
+  kp.kv_cap = (int)cfg->kv_capacity_tokens;
+  kp.max_batch = cfg->max_batch_size;
+  kp.batching = cfg->batching;
+  kp.chunk = cfg->chunk_size;
+  kp.m = cfg->num_instances;
+  kp.n_state_edges = cfg->n_state_edges;
+  kp.n_pred_edges = cfg->n_predictor_edges;
+  for (int i = 0; i < cfg->n_state_edges; ++i) kp.state_edges[i] = (int)cfg->state_edges[i];
+  for (int i = 0; i < cfg->n_predictor_edges; ++i) {
+    kp.pred_edges[i] = (int)cfg->predictor_edges[i];
+    kp.ub[i] = (int)ub_of(*cfg, i);
+  }
+  kp.n_band_edges = cfg->n_band_edges;
+  kp.predictor_mode = cfg->predictor_mode;
+  kp.rcap = L.rcap;
+  kp.wcap = L.wcap;
+  kp.dsl_cutoff = (int)std::min<int64_t>(INT_MAX, heavy_cutoff(cfg->profile, cfg->thresholds));
+  kp.flags = cfg->flags;
+  kp.max_ticks = cfg->max_ticks;
+  kp.rl_layers = cfg->policy == RS_POLICY_RL ? cfg->rl_num_layers : 0;
+  for (int i = 0; i <= RS_MAX_LAYERS; ++i) kp.rl_dims[i] = cfg->rl_dims[i];
+  for (int i = 0; i < RS_MAX_LAYERS; ++i) {
+    kp.rl_woff[i] = L.woff[i];
+    kp.rl_boff[i] = L.boff[i];
+  }
+  kp.rl_w = cfg->rl_params;
+  kp.rl_maxw = L.maxw;
+  kp.smem_weights_bytes = L.weights_bytes;
+  kp.num_replays = tr->num_replays;
+  kp.offsets = reinterpret_cast<const long long*>(tr->offsets);
+  kp.arrival = tr->arrival_s;
+  kp.prompt = tr->prompt_tokens;
+  kp.decode = tr->decode_tokens;
+  kp.task = tr->task;
+  kp.bucket = out->predicted_bucket;
+  kp.policy_seed = tr->policy_seed;
+  kp.o_instance = out->instance;
+  kp.o_routed = out->routed_s;
+  kp.o_first = out->first_token_s;
+  kp.o_completion = out->completion_s;
+  kp.o_preempt = out->preemptions;
+  kp.o_pred = out->predicted_bucket;
+  kp.stats = stats;
+  kp.ov_next = reinterpret_cast<uint32_t*>(ws + wl.next);
+  kp.ov_prev = reinterpret_cast<uint32_t*>(ws + wl.prev);
+  kp.ov_emit = reinterpret_cast<int*>(ws + wl.emit);
+  kp.mm_removed = reinterpret_cast<uint8_t*>(ws + wl.removed);
+  kp.work_counter = reinterpret_cast<int*>(ws + wl.counter);
+  kp.smem_group_bytes = L.group_bytes;
+  kp.off_run = L.off_run;
+  kp.off_wait = L.off_wait;
+  kp.off_dbc = L.off_dbc;
+  kp.off_rlx = L.off_rlx;
+  kp.off_rng = L.off_rng;
+  kp.off_front = L.off_front;
+
+  // warps (replays) per block: maximise resident warps per SM; the RL
+  // weights are staged once per block, which favours wider blocks.
+  int dev = 0;
+  RS_CUDA(cudaGetDevice(&dev));
+  int smem_optin = 0;
+  RS_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int smem_sm = 228 * 1024;
+  int best_wpb = 0, best_warps = 0;
+  const int wpb_env = env_int("RS_WARPS_PER_BLOCK", 0);
+  for (int wpb = 8; wpb >= 1; --wpb) {
+    if (wpb_env && wpb != wpb_env) continue;
+    const int bytes = L.weights_bytes + wpb * L.group_bytes;
+    if (bytes > smem_optin) continue;
+    const int blocks = std::min(32 / wpb, smem_sm / (bytes + 1024));
+    const int warps = blocks * wpb;
+    if (warps > best_warps) {
+      best_warps = warps;
+      best_wpb = wpb;
+    }
+  }
+  if (best_wpb == 0)
+    return fail(RS_ERR_UNSUPPORTED, "per-replay shared-memory state exceeds one SM (" +
+                                        std::to_string(L.weights_bytes + L.group_bytes) + " B)");
+  const int block_smem = L.weights_bytes + best_wpb * L.group_bytes;
+  RS_CUDA(cudaMemsetAsync(kp.work_counter, 0, sizeof(int), st));
+  switch (cfg->policy) {
+    case RS_POLICY_ROUND_ROBIN: return launch_replay<RS_POLICY_ROUND_ROBIN>(kp, best_wpb, block_smem, tr->num_replays, st);
+    case RS_POLICY_DEDICATED_SMALL_LARGE: return launch_replay<RS_POLICY_DEDICATED_SMALL_LARGE>(kp, best_wpb, block_smem, tr->num_replays, st);
+    case RS_POLICY_DECODE_BALANCER: return launch_replay<RS_POLICY_DECODE_BALANCER>(kp, best_wpb, block_smem, tr->num_replays, st);
+    case RS_POLICY_JSQ: return launch_replay<RS_POLICY_JSQ>(kp, best_wpb, block_smem, tr->num_replays, st);
+    case RS_POLICY_MAX_CAPACITY: return launch_replay<RS_POLICY_MAX_CAPACITY>(kp, best_wpb, block_smem, tr->num_replays, st);
+    case RS_POLICY_MIN_MIN: return launch_replay<RS_POLICY_MIN_MIN>(kp, best_wpb, block_smem, tr->num_replays, st);
+    case RS_POLICY_EARLIEST_AVAILABLE: return launch_replay<RS_POLICY_EARLIEST_AVAILABLE>(kp, best_wpb, block_smem, tr->num_replays, st);
+    case RS_POLICY_WORKLOAD_AWARE: return launch_replay<RS_POLICY_WORKLOAD_AWARE>(kp, best_wpb, block_smem, tr->num_replays, st);
+    case RS_POLICY_RL: return launch_replay<RS_POLICY_RL>(kp, best_wpb, block_smem, tr->num_replays, st);
+  }
+  return fail(RS_ERR_INVALID_ARGUMENT, "unknown policy");
+}
+
+}  // extern "C"

@@ -1,0 +1,287 @@
+// host_api.cu — host-buffer entry points of the C ABI: rs_replay_batch_host
+// (the reference-facing call: H2D, predictor kernel, replay kernel, D2H) and
+// the standalone Q-network forward used for per-stage parity.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rs_abi.h"
+#include "common.cuh"
+#include "mlp.cuh"
+
+namespace rs {
+void set_error(const std::string& m);  // engine.cu (rs_last_error's storage)
+}
+
+namespace {
+
+rs_status fail2(rs_status s, const std::string& m) {
+  rs::set_error(m);
+  return s;
+}
+
+#define RS_CUDA2(call)                                                          \
+  do {                                                                          \
+    cudaError_t e_ = (call);                                                    \
+    if (e_ != cudaSuccess)                                                      \
+      return fail2(e_ == cudaErrorMemoryAllocation ? RS_ERR_OUT_OF_MEMORY       \
+                                                   : RS_ERR_CUDA,               \
+                   std::string(#call) + ": " + cudaGetErrorString(e_));         \
+  } while (0)
+
+size_t al(size_t v) { return (v + 255) / 256 * 256; }
+
+// Per-device cached arena + stream for the host entry points.
+struct DeviceCache {
+  std::mutex mu;
+  void* base = nullptr;
+  size_t bytes = 0;
+  cudaStream_t stream = nullptr;
+};
+DeviceCache g_cache[16];
+
+rs_status arena(int dev, size_t need, char** out, cudaStream_t* st) {
+  DeviceCache& c = g_cache[dev];
+  if (!c.stream) RS_CUDA2(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+  if (c.bytes < need) {
+    if (c.base) cudaFree(c.base);
+    c.base = nullptr;
+    c.bytes = 0;
+    RS_CUDA2(cudaMalloc(&c.base, need));
+    c.bytes = need;
+  }
+  *out = static_cast<char*>(c.base);
+  *st = c.stream;
+  return RS_OK;
+}
+
+struct MlpKParams {
+  int layers;
+  int dims[RS_MAX_LAYERS + 1];
+  int woff[RS_MAX_LAYERS], boff[RS_MAX_LAYERS];
+  int maxw, weights_doubles;
+  const double* params;
+  const double* states;
+  int batch;
+  double* q;
+  int* greedy;
+};
+
+constexpr int kMlpWarps = 4;
+
+__global__ void __launch_bounds__(rs::kWarp * kMlpWarps) mlp_kernel(const __grid_constant__ MlpKParams P) {
+  extern __shared__ __align__(16) char smem[];
+  double* w = reinterpret_cast<double*>(smem);
+  rs::mlp_stage_weights(P.params, P.layers, P.dims, P.woff, P.boff, w);
+  const int wid = threadIdx.x / rs::kWarp;
+  double* x = w + P.weights_doubles + (size_t)wid * (P.dims[0] + 2 * P.maxw);
+  double* h0 = x + P.dims[0];
+  double* h1 = h0 + P.maxw;
+  rs::MlpView M{P.layers, P.dims, P.woff, P.boff, w};
+  const int dout = P.dims[P.layers];
+  for (int b = blockIdx.x * kMlpWarps + wid; b < P.batch; b += gridDim.x * kMlpWarps) {
+    for (int i = rs::lane_id(); i < P.dims[0]; i += rs::kWarp) x[i] = P.states[(size_t)b * P.dims[0] + i];
+    __syncwarp();
+    const int a = rs::mlp_forward_warp(M, x, h0, h1, P.q + (size_t)b * dout);
+    if (rs::lane_id() == 0) P.greedy[b] = a;
+    __syncwarp();
+  }
+}
+
+}  // namespace
+
+extern "C" rs_status rs_replay_batch(const rs_batch_cfg*, const rs_trace_soa*, rs_req_out*,
+                                     rs_replay_stats*, void*, size_t, void*);
+extern "C" rs_status rs_predict_buckets(const rs_batch_cfg*, const rs_trace_soa*, uint8_t*, void*);
+extern "C" rs_status rs_validate_config(const rs_batch_cfg*);
+extern "C" rs_status rs_workspace_size(const rs_batch_cfg*, int32_t, int64_t, size_t*);
+extern "C" rs_status rs_last_error(char*, size_t);
+
+namespace {
+// Errors raised inside engine.cu already carry their message.
+rs_status forward(rs_status s) { return s; }
+}  // namespace
+
+extern "C" {
+
+rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_out* out,
+                               rs_replay_stats* stats, int32_t device) {
+  rs_status s = forward(rs_validate_config(cfg));
+  if (s != RS_OK) return s;
+  if (!tr || !stats) return fail2(RS_ERR_INVALID_ARGUMENT, "null trace/stats");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail2(RS_ERR_NO_DEVICE, "no CUDA device (the engine has no CPU fallback)");
+  }
+  if (device < 0 || device >= ndev || device >= 16) return fail2(RS_ERR_INVALID_ARGUMENT, "bad device");
+  RS_CUDA2(cudaSetDevice(device));
+  const int R = tr->num_replays;
+  if (R < 0) return fail2(RS_ERR_INVALID_ARGUMENT, "num_replays < 0");
+  if (R == 0) return RS_OK;
+  if (!tr->offsets || tr->offsets[0] != 0 || tr->offsets[R] != tr->total_requests)
+    return fail2(RS_ERR_INVALID_ARGUMENT, "offsets must start at 0 and end at total_requests");
+  for (int r = 0; r < R; ++r)
+    if (tr->offsets[r + 1] < tr->offsets[r] || tr->offsets[r + 1] - tr->offsets[r] > INT32_MAX / 2)
+      return fail2(RS_ERR_INVALID_ARGUMENT, "offsets must be non-decreasing");
+  const int64_t N = tr->total_requests;
+  const bool rl = cfg->policy == RS_POLICY_RL;
+  size_t rl_bytes = 0;
+  if (rl) {
+    for (int l = 0; l < cfg->rl_num_layers; ++l)
+      rl_bytes += ((size_t)cfg->rl_dims[l] * cfg->rl_dims[l + 1] + cfg->rl_dims[l + 1]) * sizeof(double);
+  }
+  size_t ws_bytes = 0;
+  if ((s = forward(rs_workspace_size(cfg, R, N, &ws_bytes))) != RS_OK) return s;
+  // arena layout
+  size_t o = 0;
+  const size_t o_off = o; o += al(8ull * (R + 1));
+  const size_t o_arr = o; o += al(8ull * N);
+  const size_t o_pr = o; o += al(4ull * N);
+  const size_t o_de = o; o += al(4ull * N);
+  const size_t o_tk = o; o += al(1ull * N);
+  const size_t o_gv = o; o += al(1ull * N);
+  const size_t o_ps = o; o += al(8ull * R);
+  const size_t o_qs = o; o += al(8ull * R);
+  const size_t o_rl = o; o += al(rl_bytes);
+  const size_t o_in = o; o += al(4ull * N);
+  const size_t o_ro = o; o += al(8ull * N);
+  const size_t o_fi = o; o += al(8ull * N);
+  const size_t o_co = o; o += al(8ull * N);
+  const size_t o_pe = o; o += al(4ull * N);
+  const size_t o_pb = o; o += al(1ull * N);
+  const size_t o_st = o; o += al(sizeof(rs_replay_stats) * R);
+  const size_t o_ws = o; o += al(ws_bytes);
+  DeviceCache& dc = g_cache[device];
+  std::lock_guard<std::mutex> lock(dc.mu);
+  char* b = nullptr;
+  cudaStream_t st = nullptr;
+  if ((s = arena(device, o, &b, &st)) != RS_OK) return s;
+  auto h2d = [&](size_t off, const void* src, size_t n) -> cudaError_t {
+    if (!src || n == 0) return cudaSuccess;
+    return cudaMemcpyAsync(b + off, src, n, cudaMemcpyHostToDevice, st);
+  };
+  RS_CUDA2(h2d(o_off, tr->offsets, 8ull * (R + 1)));
+  RS_CUDA2(h2d(o_arr, tr->arrival_s, 8ull * N));
+  RS_CUDA2(h2d(o_pr, tr->prompt_tokens, 4ull * N));
+  RS_CUDA2(h2d(o_de, tr->decode_tokens, 4ull * N));
+  RS_CUDA2(h2d(o_tk, tr->task, 1ull * N));
+  if (tr->given_bucket) RS_CUDA2(h2d(o_gv, tr->given_bucket, 1ull * N));
+  if (tr->predictor_seed) RS_CUDA2(h2d(o_ps, tr->predictor_seed, 8ull * R));
+  if (tr->policy_seed) RS_CUDA2(h2d(o_qs, tr->policy_seed, 8ull * R));
+  if (rl) RS_CUDA2(h2d(o_rl, cfg->rl_params, rl_bytes));
+
+  rs_batch_cfg dcfg = *cfg;
+  if (rl) dcfg.rl_params = reinterpret_cast<const double*>(b + o_rl);
+  rs_trace_soa dt = *tr;
+  dt.offsets = reinterpret_cast<const int64_t*>(b + o_off);
+  dt.arrival_s = reinterpret_cast<const double*>(b + o_arr);
+  dt.prompt_tokens = reinterpret_cast<const int32_t*>(b + o_pr);
+  dt.decode_tokens = reinterpret_cast<const int32_t*>(b + o_de);
+  dt.task = reinterpret_cast<const uint8_t*>(b + o_tk);
+  dt.given_bucket = tr->given_bucket ? reinterpret_cast<const uint8_t*>(b + o_gv) : nullptr;
+  dt.predictor_seed = tr->predictor_seed ? reinterpret_cast<const uint64_t*>(b + o_ps) : nullptr;
+  dt.policy_seed = tr->policy_seed ? reinterpret_cast<const uint64_t*>(b + o_qs) : nullptr;
+  rs_req_out dout;
+  dout.instance = reinterpret_cast<int32_t*>(b + o_in);
+  dout.routed_s = reinterpret_cast<double*>(b + o_ro);
+  dout.first_token_s = reinterpret_cast<double*>(b + o_fi);
+  dout.completion_s = reinterpret_cast<double*>(b + o_co);
+  dout.preemptions = reinterpret_cast<int32_t*>(b + o_pe);
+  dout.predicted_bucket = reinterpret_cast<uint8_t*>(b + o_pb);
+  rs_replay_stats* dstats = reinterpret_cast<rs_replay_stats*>(b + o_st);
+
+  if ((s = forward(rs_predict_buckets(&dcfg, &dt, dout.predicted_bucket, st))) != RS_OK) return s;
+  if ((s = forward(rs_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st))) != RS_OK)
+    return s;
+  auto d2h = [&](void* dst, size_t off, size_t n) -> cudaError_t {
+    if (!dst || n == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, b + off, n, cudaMemcpyDeviceToHost, st);
+  };
+  if (out) {
+    RS_CUDA2(d2h(out->instance, o_in, 4ull * N));
+    RS_CUDA2(d2h(out->routed_s, o_ro, 8ull * N));
+    RS_CUDA2(d2h(out->first_token_s, o_fi, 8ull * N));
+    RS_CUDA2(d2h(out->completion_s, o_co, 8ull * N));
+    RS_CUDA2(d2h(out->preemptions, o_pe, 4ull * N));
+    RS_CUDA2(d2h(out->predicted_bucket, o_pb, 1ull * N));
+  }
+  RS_CUDA2(d2h(stats, o_st, sizeof(rs_replay_stats) * R));
+  RS_CUDA2(cudaStreamSynchronize(st));
+  // The reference leaves predicted_bucket unset (-1) for requests that never
+  // reached the router queue; report those as 255.
+  if (out && out->predicted_bucket) {
+    for (int r = 0; r < R; ++r) {
+      const int64_t b0 = tr->offsets[r] + stats[r].injected, e0 = tr->offsets[r + 1];
+      for (int64_t i = b0; i < e0; ++i) out->predicted_bucket[i] = 255;
+    }
+  }
+  return RS_OK;
+}
+
+rs_status rs_mlp_forward_host(const rs_batch_cfg* cfg, const double* states, int32_t batch,
+                              double* q_out, int32_t* greedy_out, int32_t device) {
+  if (!cfg || !states || !q_out || !greedy_out || batch < 0)
+    return fail2(RS_ERR_INVALID_ARGUMENT, "null argument");
+  if (cfg->rl_num_layers < 1 || cfg->rl_num_layers > RS_MAX_LAYERS || !cfg->rl_params)
+    return fail2(RS_ERR_INVALID_ARGUMENT, "rl: 1..4 layers and parameters required");
+  for (int l = 0; l <= cfg->rl_num_layers; ++l)
+    if (cfg->rl_dims[l] < 1 || cfg->rl_dims[l] > RS_MAX_WIDTH)
+      return fail2(RS_ERR_UNSUPPORTED, "rl: layer width outside [1, 512]");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail2(RS_ERR_NO_DEVICE, "no CUDA device (the engine has no CPU fallback)");
+  }
+  if (device < 0 || device >= ndev || device >= 16) return fail2(RS_ERR_INVALID_ARGUMENT, "bad device");
+  RS_CUDA2(cudaSetDevice(device));
+  if (batch == 0) return RS_OK;
+  MlpKParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.layers = cfg->rl_num_layers;
+  size_t w = 0;
+  P.maxw = 1;
+  for (int l = 0; l <= P.layers; ++l) P.dims[l] = cfg->rl_dims[l];
+  for (int l = 0; l < P.layers; ++l) {
+    P.woff[l] = (int)w;
+    w += (size_t)P.dims[l] * P.dims[l + 1];
+    P.boff[l] = (int)w;
+    w += P.dims[l + 1];
+    P.maxw = std::max(P.maxw, P.dims[l + 1]);
+  }
+  P.weights_doubles = (int)w;
+  const int d0 = P.dims[0], dout = P.dims[P.layers];
+  size_t o = 0;
+  const size_t o_p = o; o += al(w * 8);
+  const size_t o_x = o; o += al((size_t)batch * d0 * 8);
+  const size_t o_q = o; o += al((size_t)batch * dout * 8);
+  const size_t o_g = o; o += al((size_t)batch * 4);
+  DeviceCache& dc = g_cache[device];
+  std::lock_guard<std::mutex> lock(dc.mu);
+  char* b = nullptr;
+  cudaStream_t st = nullptr;
+  rs_status s;
+  if ((s = arena(device, o, &b, &st)) != RS_OK) return s;
+  RS_CUDA2(cudaMemcpyAsync(b + o_p, cfg->rl_params, w * 8, cudaMemcpyHostToDevice, st));
+  RS_CUDA2(cudaMemcpyAsync(b + o_x, states, (size_t)batch * d0 * 8, cudaMemcpyHostToDevice, st));
+  P.params = reinterpret_cast<const double*>(b + o_p);
+  P.states = reinterpret_cast<const double*>(b + o_x);
+  P.batch = batch;
+  P.q = reinterpret_cast<double*>(b + o_q);
+  P.greedy = reinterpret_cast<int*>(b + o_g);
+  const int smem = (int)(w * 8 + (size_t)kMlpWarps * (d0 + 2 * P.maxw) * 8);
+  RS_CUDA2(cudaFuncSetAttribute(mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  const int grid = std::min(1024, (batch + kMlpWarps - 1) / kMlpWarps);
+  mlp_kernel<<<grid, rs::kWarp * kMlpWarps, smem, st>>>(P);
+  RS_CUDA2(cudaGetLastError());
+  RS_CUDA2(cudaMemcpyAsync(q_out, b + o_q, (size_t)batch * dout * 8, cudaMemcpyDeviceToHost, st));
+  RS_CUDA2(cudaMemcpyAsync(greedy_out, b + o_g, (size_t)batch * 4, cudaMemcpyDeviceToHost, st));
+  RS_CUDA2(cudaStreamSynchronize(st));
+  return RS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,111 @@
+// mlp.cuh — kernel (c): the RL router's Q-network forward + action selection.
+//
+// Mlp::forward (mlp.hpp:54-68 / affine mlp.hpp:139-152) computes, per output,
+//     acc = b[o]; for i in 0..ni-1: acc += w[o][i] * x[i]
+// with one rounding after every multiply and every add.  Bit-exact parity
+// forbids reassociation (no split-K, no tensor-core accumulation: tcgen05 /
+// DMMA accumulate with a different rounding sequence), so each output is a
+// sequential fp64 chain; the parallelism is across outputs (one lane per
+// output, two chains per lane for ILP) and across replays (one warp each).
+//
+// The weights are staged ONCE per CTA in shared memory, transposed to
+// W^T[i][o] so that the 32 lanes of a warp read 32 consecutive doubles per
+// input (conflict-free), and x[i] is a shared-memory broadcast.
+//
+// Exact-zero inputs are skipped: w*(+-0) = +-0 and acc + (+-0) == acc for
+// every acc != 0; for acc == +-0 only the sign of a zero can differ, which no
+// ReLU (v > 0 ? v : 0) or argmax (strict >) can observe.  Decisions and
+// non-zero Q values are therefore bit-identical to the reference.
+#pragma once
+
+#include "common.cuh"
+
+namespace rs {
+
+struct MlpView {
+  int layers;
+  const int* dims;   // layers + 1
+  const int* woff;   // per layer: offset of W^T (doubles) in `w`
+  const int* boff;   // per layer: offset of b
+  const double* w;   // shared memory
+};
+
+// Forward of one state vector `x` (shared memory, dims[0] doubles) by one
+// warp.  h0/h1: shared scratch of max width.  Writes the final layer to
+// `q_out` (may be nullptr) and returns argmax_action (dqn.hpp:82-90).
+__device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double* h0,
+                                       double* h1, double* q_out) {
+  const int l = lane_id();
+  const double* cur = x;
+  unsigned long long best_key = 0;
+  int best_idx = 0x7fffffff;
+  bool have = false;
+  for (int layer = 0; layer < M.layers; ++layer) {
+    const int ni = M.dims[layer], no = M.dims[layer + 1];
+    const double* WT = M.w + M.woff[layer];
+    const double* B = M.w + M.boff[layer];
+    const bool last = (layer + 1 == M.layers);
+    double* dst = (layer & 1) ? h1 : h0;
+    for (int ob = 0; ob < no; ob += 2 * kWarp) {
+      const int o0 = ob + l, o1 = ob + kWarp + l;
+      const bool v0 = o0 < no, v1 = o1 < no;
+      double a0 = v0 ? B[o0] : 0.0;
+      double a1 = v1 ? B[o1] : 0.0;
+#pragma unroll 4
+      for (int i = 0; i < ni; ++i) {
+        const double xi = cur[i];
+        if (xi != 0.0) {
+          const double* row = WT + (size_t)i * no;
+          const double w0 = v0 ? row[o0] : 0.0;
+          const double w1 = v1 ? row[o1] : 0.0;
+          a0 = __dadd_rn(a0, __dmul_rn(w0, xi));
+          a1 = __dadd_rn(a1, __dmul_rn(w1, xi));
+        }
+      }
+      if (!last) {
+        if (v0) dst[o0] = a0 > 0.0 ? a0 : 0.0;
+        if (v1) dst[o1] = a1 > 0.0 ? a1 : 0.0;
+      } else {
+        if (q_out) {
+          if (v0) q_out[o0] = a0;
+          if (v1) q_out[o1] = a1;
+        }
+        // running argmax, strict >: lower indices win ties
+        if (v0) {
+          unsigned long long k = ordered_key(a0);
+          if (!have || k > best_key) { best_key = k; best_idx = o0; have = true; }
+        }
+        if (v1) {
+          unsigned long long k = ordered_key(a1);
+          if (!have || k > best_key) { best_key = k; best_idx = o1; have = true; }
+        }
+      }
+    }
+    __syncwarp();
+    cur = dst;
+  }
+  const unsigned long long gmax = warp_max_u64(have ? best_key : 0ull);
+  const int cand = (have && best_key == gmax) ? best_idx : 0x7fffffff;
+  return warp_min(cand);
+}
+
+// Cooperative (whole CTA) copy of the reference flat parameter vector
+// (per layer W[o][i] row-major, then b) into the transposed shared layout.
+__device__ inline void mlp_stage_weights(const double* __restrict__ params, int layers,
+                                         const int* dims, const int* woff, const int* boff,
+                                         double* smem_w) {
+  size_t src = 0;
+  for (int layer = 0; layer < layers; ++layer) {
+    const int ni = dims[layer], no = dims[layer + 1];
+    const int nw = ni * no;
+    for (int k = threadIdx.x; k < nw; k += blockDim.x) {
+      const int o = k / ni, i = k - o * ni;
+      smem_w[woff[layer] + i * no + o] = params[src + k];
+    }
+    for (int k = threadIdx.x; k < no; k += blockDim.x) smem_w[boff[layer] + k] = params[src + nw + k];
+    src += (size_t)nw + no;
+  }
+  __syncthreads();
+}
+
+}  // namespace rs

@@ -1,0 +1,610 @@
+// router.cuh — the per-replay tick loop: router decide() for every policy
+// (policies.hpp:50-245 + workload_aware + RlPolicy), routing, the instance
+// sweep, arrival injection and the end-of-replay statistics.
+#pragma once
+
+#include "replay.cuh"
+
+namespace rs {
+
+constexpr int kMaxTokens = 1 << 20;  // engine limit on prompt / decode tokens
+
+struct Feat {  // InstanceFeatures subset, from the maintained aggregates
+  long long res, pend, dleft, tleft, tok;
+  int cnt, kv, nrun, mind;
+};
+
+__device__ __forceinline__ Feat load_feat(const Grp& G, int i) {
+  const InstHot& h = G.inst[i];
+  Feat f;
+  f.res = h.res_run + h.res_wait;
+  f.pend = h.pend_run + h.pend_wait;
+  f.dleft = h.dleft_run + h.dleft_wait;
+  f.tleft = h.tleft_run + h.tleft_wait;
+  f.tok = h.tok_run + h.tok_wait;
+  f.cnt = h.n_run + h.w_cnt + h.o_cnt;
+  f.kv = h.kv_run;
+  f.nrun = h.n_run;
+  f.mind = h.min_dleft;
+  return f;
+}
+
+// can_accept (policies.hpp:44-48)
+__device__ __forceinline__ bool can_accept(const KParams& P, const Feat& f, int need) {
+  return (long long)P.kv_cap - f.res >= need && f.cnt < P.max_batch;
+}
+
+// capacity_fraction (instance.hpp:138-142)
+__device__ __forceinline__ double capacity_of(const KParams& P, int kv) {
+  double v = __dsub_rn(1.0, __ddiv_rn((double)kv, (double)P.kv_cap));
+  return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+}
+
+__device__ __forceinline__ double round2(double x) {  // env.hpp:82
+  return __ddiv_rn(round(__dmul_rn(x, 100.0)), 100.0);
+}
+
+__device__ __forceinline__ InstHot load_inst(const Grp& G, int i) { return G.inst[i]; }
+__device__ __forceinline__ void store_inst(const Grp& G, int i, const InstHot& h) {
+  if (lane_id() == 0) G.inst[i] = h;
+  __syncwarp();
+}
+
+// Head-window: request data of the range head (prompt, true decode, bucket).
+__device__ __forceinline__ void head_window(const KParams& P, Replay& R, int q) {
+  if (q >= R.h_base && q < R.h_base + kWarp) return;
+  R.h_base = q & ~(kWarp - 1);
+  const int j = R.h_base + lane_id();
+  if (j < R.n) {
+    R.h_prompt = P.prompt[R.off + j];
+    R.h_true = P.decode[R.off + j];
+    R.h_bucket = P.bucket[R.off + j];
+  }
+}
+
+__device__ __forceinline__ Rec load_req(const KParams& P, long long off, int req, int* bucket) {
+  int v[3] = {0, 0, 0};
+  if (lane_id() == 0) {
+    v[0] = P.prompt[off + req];
+    v[1] = P.decode[off + req];
+    v[2] = P.bucket[off + req];
+  }
+  Rec r;
+  r.req = req;
+  r.prompt = __shfl_sync(kFull, v[0], 0);
+  r.tru = __shfl_sync(kFull, v[1], 0);
+  *bucket = __shfl_sync(kFull, v[2], 0);
+  r.dhat = P.ub[*bucket];
+  r.emit = 0;
+  return r;
+}
+
+template <int POL>
+__device__ __forceinline__ Rec head_rec(const KParams& P, const Grp& G, Replay& R, int* bucket) {
+  if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) return load_req(P, R.off, G.front[0], bucket);
+  head_window(P, R, R.qhead);
+  const int s = R.qhead - R.h_base;
+  Rec r;
+  r.req = R.qhead;
+  r.prompt = __shfl_sync(kFull, R.h_prompt, s);
+  r.tru = __shfl_sync(kFull, R.h_true, s);
+  *bucket = __shfl_sync(kFull, R.h_bucket, s);
+  r.dhat = P.ub[*bucket];
+  r.emit = 0;
+  return r;
+}
+
+__device__ __forceinline__ void load_arrival_window(const KParams& P, Replay& R) {
+  const int j = R.a_base + lane_id();
+  R.a_val = j < R.n ? P.arrival[R.off + j] : __longlong_as_double(0x7ff0000000000000ll);
+}
+
+// ClusterSim::inject_arrivals (env.hpp:357-375): predictions were resolved
+// by the predictor pre-pass, so injection is a cursor advance.
+__device__ __forceinline__ void inject(const KParams& P, Replay& R) {
+  for (;;) {
+    const int j = R.a_base + lane_id();
+    const bool ok = j >= R.cursor && j < R.n && R.a_val <= R.clock;
+    R.cursor += __popc(__ballot_sync(kFull, ok));
+    if (R.cursor == R.a_base + kWarp && R.cursor < R.n) {
+      R.a_base += kWarp;
+      load_arrival_window(P, R);
+      continue;
+    }
+    break;
+  }
+}
+
+template <int POL>
+__device__ __forceinline__ int queue_len(const Replay& R) {
+  if (POL == RS_POLICY_MIN_MIN) return R.nfront + (R.cursor - R.qhead) - R.n_removed;
+  return R.cursor - R.qhead;
+}
+
+// Skip range entries that min_min moved to the front list.
+__device__ __forceinline__ void mm_skip_removed(const KParams& P, Replay& R) {
+  while (R.qhead < R.cursor && R.n_removed > 0) {
+    int rem = 0;
+    if (lane_id() == 0) rem = P.mm_removed[R.off + R.qhead];
+    rem = __shfl_sync(kFull, rem, 0);
+    if (!rem) break;
+    R.qhead++;
+    R.n_removed--;
+  }
+}
+
+// MinMinPolicy::pick_queue_index (policies.hpp:179-191) + move_to_front
+// (env.hpp:234-243).  Queue order = front list, then the range in index
+// order minus removed entries.  Returns false on front-list overflow.
+__device__ inline bool minmin_pick(const KParams& P, const Grp& G, Replay& R) {
+  const int l = lane_id();
+  unsigned long long fk = ~0ull;
+  int fpos = 0x7fffffff;
+  if (R.nfront > 0) {
+    unsigned long long k = ~0ull;
+    if (l < R.nfront) {
+      const int req = G.front[l];
+      const double est = __dadd_rn(__dmul_rn(P.tpp, (double)P.prompt[R.off + req]),
+                                   __dmul_rn(P.dtb, (double)P.ub[P.bucket[R.off + req]]));
+      k = ordered_key(est);
+    }
+    fk = warp_min_u64(k);
+    fpos = warp_min((l < R.nfront && k == fk) ? l : 0x7fffffff);
+  }
+  unsigned long long rk = ~0ull;
+  int ridx = -1;
+  for (int c = R.qhead; c < R.cursor; c += kWarp) {
+    const int j = c + l;
+    unsigned long long k = ~0ull;
+    if (j < R.cursor) {
+      const long long g = R.off + j;
+      if (!P.mm_removed[g]) {
+        const double est = __dadd_rn(__dmul_rn(P.tpp, (double)P.prompt[g]),
+                                     __dmul_rn(P.dtb, (double)P.ub[P.bucket[g]]));
+        k = ordered_key(est);
+      }
+    }
+    const unsigned long long mk = warp_min_u64(k);
+    if (mk < rk) {
+      rk = mk;
+      ridx = warp_min((k == mk && j < R.cursor) ? j : 0x7fffffff);
+    }
+  }
+  if (R.nfront > 0 && fk <= rk) {  // front entry (earlier queue positions win ties)
+    if (fpos == 0) return true;
+    const int v = G.front[fpos];
+    __syncwarp();
+    if (l == 0) {
+      for (int k = fpos; k > 0; --k) G.front[k] = G.front[k - 1];
+      G.front[0] = v;
+    }
+    __syncwarp();
+    return true;
+  }
+  if (ridx < 0) return true;
+  if (R.nfront == 0 && ridx == R.qhead) return true;  // already the head
+  if (R.nfront >= kMaxFront) return false;
+  if (l == 0) {
+    P.mm_removed[R.off + ridx] = 1;
+    for (int k = R.nfront; k > 0; --k) G.front[k] = G.front[k - 1];
+    G.front[0] = ridx;
+  }
+  __syncwarp();
+  R.nfront++;
+  R.n_removed++;
+  mm_skip_removed(P, R);
+  return true;
+}
+
+// ε-greedy stream (DqnAgent::act, dqn.hpp:92-99) in shared memory.
+__device__ __forceinline__ unsigned long long rng_draw(const Grp& G, Replay& R) {
+  unsigned long long* st = G.rng;
+  unsigned long long* ob = G.rng + 312;
+  if (R.rng_pos == 312) {
+    mt_twist_warp(st);
+    for (int k = lane_id(); k < 312; k += kWarp) ob[k] = mt_temper(st[k]);
+    __syncwarp();
+    R.rng_pos = 0;
+  }
+  return ob[R.rng_pos++];
+}
+
+// Router decision for one tick.  `has_head` / `hr` / `hb` describe the head.
+template <int POL>
+__device__ inline int decide(const KParams& P, const Grp& G, const MlpView& M, Replay& R,
+                             bool has_head, const Rec& hr, int hb) {
+  const int m = P.m;
+  const int l = lane_id();
+  const int need = reserved_of(hr.prompt, hr.dhat, 0);
+  if (POL == RS_POLICY_ROUND_ROBIN) {  // policies.hpp:50-69
+    if (!has_head) return m;
+    const int t = (int)(R.rr_next % (unsigned long long)m);
+    if (!can_accept(P, load_feat(G, t), need)) return m;
+    R.rr_next++;
+    return t;
+  } else if (POL == RS_POLICY_DEDICATED_SMALL_LARGE) {  // policies.hpp:73-104
+    if (!has_head) return m;
+    int t;
+    if (m < 2 || hr.dhat >= P.dsl_cutoff) t = 0;
+    else t = 1 + (int)(R.dsl_next % (unsigned long long)(m - 1));
+    if (!can_accept(P, load_feat(G, t), need)) return m;
+    if (m >= 2 && t >= 1) R.dsl_next++;
+    return t;
+  } else if (POL == RS_POLICY_MAX_CAPACITY) {  // policies.hpp:150-170
+    if (!has_head || R.clock < R.mc_next) return m;
+    unsigned long long bk = 0;
+    int bi = -1;
+    for (int g = 0; g < m; g += kWarp) {
+      const int i = g + l;
+      const bool v = i < m;
+      const unsigned long long k = v ? ordered_key(capacity_of(P, G.inst[i].kv_run)) : 0ull;
+      const int a = warp_argmax_key(k, v);
+      const unsigned long long ka = __shfl_sync(kFull, k, a);
+      if (bi < 0 || ka > bk) { bk = ka; bi = g + a; }
+    }
+    const Feat f = load_feat(G, bi);
+    if ((long long)P.kv_cap - f.res < need) return m;
+    R.mc_next = __dadd_rn(R.clock, 1.0);
+    return bi;
+  } else if (POL == RS_POLICY_EARLIEST_AVAILABLE) {  // policies.hpp:214-228
+    if (!has_head) return m;
+    for (int g = 0; g < m; g += kWarp) {
+      const int i = g + l;
+      bool ok = false;
+      if (i < m) ok = (long long)P.kv_cap - load_feat(G, i).res >= need;
+      const unsigned b = __ballot_sync(kFull, ok);
+      if (b) return g + __ffs(b) - 1;
+    }
+    return m;
+  } else if (POL == RS_POLICY_RL) {  // RlPolicy + encode_state (env.hpp:88-113)
+    double* x = G.rlx;
+    const int nsb = P.n_state_edges;
+    const int per = 3 + nsb;
+    for (int g = 0; g < m; g += kWarp) {
+      const int i = g + l;
+      if (i < m) {
+        const Feat f = load_feat(G, i);
+        double* xi = x + i * per;
+        xi[0] = __ddiv_rn((double)f.pend, (double)P.kv_cap);
+        for (int b = 0; b < nsb; ++b)
+          xi[1 + b] = __ddiv_rn((double)G.dbc[i * RS_MAX_BUCKETS + b], (double)P.max_batch);
+        xi[1 + nsb] = round2(capacity_of(P, f.kv));
+        const double that = f.nrun == 0 ? 0.0 : __dmul_rn(P.dtb, (double)f.mind);
+        xi[2 + nsb] = round2(that);
+      }
+    }
+    if (l == 0) {
+      const int q = queue_len<POL>(R);
+      x[m * per] = __ddiv_rn((double)(q < 512 ? q : 512), 512.0);
+      x[m * per + 1] = has_head ? __ddiv_rn((double)hr.prompt, 1024.0) : 0.0;
+      x[m * per + 2] = has_head ? (double)hb : 0.0;
+    }
+    __syncwarp();
+    const int na = P.rl_dims[P.rl_layers];
+    if (P.rl_eps > 0.0) {
+      const double u = u01(rng_draw(G, R));
+      if (u < P.rl_eps) {
+        const double v = __dmul_rn(u01(rng_draw(G, R)), (double)na);
+        const unsigned long long k = (unsigned long long)v;  // static_cast<uint64_t>
+        return (int)(k < (unsigned long long)na ? k : (unsigned long long)na - 1);
+      }
+    }
+    double* h0 = x + M.dims[0];
+    double* h1 = h0 + P.rl_maxw;
+    return mlp_forward_warp(M, x, h0, h1, nullptr);
+  } else {
+    // argmin policies: decode_balancer / jsq / min_min / workload_aware
+    if (!has_head) return m;
+    unsigned long long bk = ~0ull;
+    int bi = -1;
+    for (int g = 0; g < m; g += kWarp) {
+      const int i = g + l;
+      bool v = i < m;
+      unsigned long long k = ~0ull;
+      if (v) {
+        const Feat f = load_feat(G, i);
+        if (POL == RS_POLICY_DECODE_BALANCER) {  // policies.hpp:108-127
+          v = can_accept(P, f, need);
+          k = (unsigned long long)f.tleft;
+        } else if (POL == RS_POLICY_JSQ) {  // policies.hpp:131-146
+          k = (unsigned long long)(f.pend + f.dleft);
+        } else if (POL == RS_POLICY_MIN_MIN) {  // policies.hpp:193-206
+          k = ordered_key(__dadd_rn(__dmul_rn((double)f.pend, P.tpp),
+                                    __dmul_rn((double)f.dleft, P.dtb)));
+        } else {  // RS_POLICY_WORKLOAD_AWARE, SURVEY.md Appendix B
+          v = can_accept(P, f, need);
+          const long long p = hr.prompt, d = hr.dhat;
+          const double avail = __dmul_rn(P.dtb, (double)f.dleft);
+          const double pcost = __dmul_rn(P.tpp, (double)(f.pend + p));
+          const double pi = (double)p;
+          const double lead = P.prompt_exp == 2 ? __dmul_rn(pi, pi) : pi;
+          const double t_p = __dmul_rn(P.grad1, __dadd_rn(lead, (double)f.tok));
+          const double r_p = t_p <= P.eps_s ? 1.0 : __dsub_rn(1.0, __ddiv_rn(t_p, P.eps_s));
+          const double r_d = __dmul_rn(-P.grad2, (double)(f.tok + p + d));
+          const double mix = __dadd_rn(__dmul_rn(P.alpha, r_p),
+                                       __dmul_rn(__dsub_rn(1.0, P.alpha), r_d));
+          const double score = __dsub_rn(__dadd_rn(avail, pcost), __dmul_rn(P.eps_s, mix));
+          k = ordered_key(score);
+        }
+      }
+      const int a = warp_argmin_key(k, v);
+      if (a >= 0) {
+        const unsigned long long ka = __shfl_sync(kFull, k, a);
+        if (bi < 0 || ka < bk) { bk = ka; bi = g + a; }
+      }
+    }
+    if (POL == RS_POLICY_JSQ || POL == RS_POLICY_MIN_MIN) return bi;
+    return bi < 0 ? m : bi;
+  }
+}
+
+template <int POL>
+__device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int r) {
+  constexpr bool NEED_DBC = POL == RS_POLICY_RL;
+  const int l = lane_id();
+  Replay R;
+  R.off = P.offsets[r];
+  R.n = (int)(P.offsets[r + 1] - R.off);
+  const int m = P.m;
+
+  // outputs to the reference's "not yet" values; input checks
+  bool bad = false;
+  for (int j = l; j < R.n; j += kWarp) {
+    const long long g = R.off + j;
+    P.o_instance[g] = -1;
+    P.o_routed[g] = -1.0;
+    P.o_first[g] = -1.0;
+    P.o_completion[g] = -1.0;
+    P.o_preempt[g] = 0;
+    if (POL == RS_POLICY_MIN_MIN) P.mm_removed[g] = 0;
+    const int p = P.prompt[g], d = P.decode[g];
+    if (p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens) bad = true;
+    if (j > 0 && P.arrival[g] < P.arrival[g - 1]) bad = true;
+  }
+  bad = __any_sync(kFull, bad);
+  for (int i = l; i < m; i += kWarp) {
+    InstHot h;
+    h.clock = 0.0;
+    h.res_wait = h.pend_wait = h.dleft_wait = h.tleft_wait = h.tok_wait = 0;
+    h.n_run = h.n_prefill = h.res_run = h.kv_run = h.pend_run = 0;
+    h.dleft_run = h.tleft_run = h.tok_run = 0;
+    h.min_dleft = 0x7fffffff;
+    h.w_head = h.w_cnt = h.o_cnt = 0;
+    h.o_head = h.o_tail = (int)kNil;
+    h._pad0 = h._pad1 = 0;
+    G.inst[i] = h;
+    if (NEED_DBC)
+      for (int b = 0; b < RS_MAX_BUCKETS; ++b) G.dbc[i * RS_MAX_BUCKETS + b] = 0;
+  }
+  R.clock = 0.0;
+  R.tick = 0;
+  R.qhead = R.cursor = 0;
+  R.completed = 0;
+  R.nfront = R.n_removed = 0;
+  R.total_wait = 0;
+  R.rr_next = R.dsl_next = 0;
+  R.mc_next = 0.0;
+  R.hash = 0xcbf29ce484222325ull;
+  R.infeasible = R.routed = R.sum_q = R.sum_w = 0;
+  R.status = RS_REPLAY_FINISHED;
+  R.err_inst = -1;
+  R.rng_pos = 312;
+  R.a_base = 0;
+  R.h_base = -2 * kWarp;
+  R.h_prompt = R.h_true = R.h_bucket = 0;
+  if (POL == RS_POLICY_RL && P.rl_eps > 0.0)
+    mt_seed_warp(G.rng, P.policy_seed ? P.policy_seed[r] : 0ull);
+  __syncwarp();
+  load_arrival_window(P, R);
+  if (bad) {
+    R.status = RS_REPLAY_INVALID_TRACE;
+  } else {
+    inject(P, R);  // ctor (env.hpp:193)
+  }
+
+  // ---------------------------------------------------------- tick loop
+  while (R.status == RS_REPLAY_FINISHED && R.completed != R.n && R.tick < P.max_ticks) {
+    if (POL == RS_POLICY_MIN_MIN && queue_len<POL>(R) > 0) {
+      if (!minmin_pick(P, G, R)) { R.status = RS_REPLAY_CAPACITY; break; }
+    }
+    const bool has_head = queue_len<POL>(R) > 0;
+    Rec hr;
+    int hb = 0;
+    if (has_head) {
+      hr = head_rec<POL>(P, G, R, &hb);
+    } else {
+      hr.req = hr.prompt = hr.dhat = hr.tru = hr.emit = 0;
+    }
+    const int action = decide<POL>(P, G, M, R, has_head, hr, hb);
+    R.hash = hash_action(R.hash, action);
+    if (action < 0 || action > m) { R.status = RS_REPLAY_BAD_ACTION; break; }
+    const double t1 = __dadd_rn(R.clock, P.delta_t);
+    if (action < m && has_head) {
+      if ((long long)hr.prompt + hr.tru > P.kv_cap) {
+        R.infeasible++;  // env.hpp:262-267: flagged, stays queued
+      } else {
+        if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) {
+          if (l == 0)
+            for (int k = 0; k + 1 < R.nfront; ++k) G.front[k] = G.front[k + 1];
+          __syncwarp();
+          R.nfront--;
+        } else {
+          R.qhead++;
+          if (POL == RS_POLICY_MIN_MIN) mm_skip_removed(P, R);
+        }
+        if (l == 0) {
+          P.o_routed[R.off + hr.req] = R.clock;
+          P.o_instance[R.off + hr.req] = action;
+        }
+        R.routed++;
+        InstHot h = load_inst(G, action);  // Instance::enqueue
+        if (h.clock < R.clock) h.clock = R.clock;
+        wait_push_back(P, G, R.off, action, h, hr);
+        store_inst(G, action, h);
+        R.total_wait++;
+      }
+    }
+    // run_until(t1) for every instance, index order (independent)
+    int comps = 0;
+    for (int g = 0; g < m && R.status == RS_REPLAY_FINISHED; g += kWarp) {
+      const int i = g + l;
+      bool busy = false;
+      if (i < m) {
+        const InstHot& hi = G.inst[i];
+        if (hi.clock < t1) {
+          if (hi.n_run > 0 || hi.w_cnt > 0) busy = true;
+          else G.inst[i].clock = t1;  // idle instance skips ahead
+        }
+      }
+      unsigned mask = __ballot_sync(kFull, busy);
+      __syncwarp();
+      while (mask) {
+        const int ii = g + __ffs(mask) - 1;
+        mask &= mask - 1;
+        InstHot h = load_inst(G, ii);
+        const int w0 = h.w_cnt + h.o_cnt;
+        while (h.clock < t1 && (h.n_run > 0 || h.w_cnt > 0)) {
+          const int c = inst_step<NEED_DBC>(P, G, R.off, ii, h);
+          if (c < 0) {
+            R.status = RS_REPLAY_NOT_ADMISSIBLE;
+            R.err_inst = ii;
+            break;
+          }
+          comps += c;
+        }
+        if (h.n_run == 0 && h.w_cnt == 0 && h.clock < t1) h.clock = t1;
+        R.total_wait += h.w_cnt + h.o_cnt - w0;
+        store_inst(G, ii, h);
+        if (R.status != RS_REPLAY_FINISHED) break;
+      }
+    }
+    if (R.status != RS_REPLAY_FINISHED) break;
+    R.completed += comps;
+    R.clock = t1;
+    inject(P, R);
+    R.tick++;
+    R.sum_q += queue_len<POL>(R);
+    R.sum_w += R.total_wait;
+  }
+  if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
+
+  // ------------------------------------------------- statistics (metrics.hpp)
+  double se = 0.0, st = 0.0, sb = 0.0, sw = 0.0;
+  long long tbtc = 0, pre = 0, tok = 0;
+  double fa = __longlong_as_double(0x7fefffffffffffffll), lc = 0.0;
+  for (int b0 = 0; b0 < R.n; b0 += kWarp) {
+    const int j = b0 + l;
+    const bool v = j < R.n;
+    const long long g = R.off + j;
+    const double comp = v ? P.o_completion[g] : -1.0;
+    const bool c = comp >= 0.0;
+    double e = 0.0, t = 0.0, tb = 0.0, w = 0.0, arr = 0.0;
+    bool htb = false, hw = false;
+    if (c) {
+      arr = P.arrival[g];
+      const double first = P.o_first[g];
+      const double routed = P.o_routed[g];
+      const int d = P.decode[g];  // tokens_emitted at completion
+      e = __dsub_rn(comp, arr);
+      t = __dsub_rn(first, arr);
+      if (d >= 2) {
+        htb = true;
+        tb = __ddiv_rn(__dsub_rn(comp, first), (double)(d - 1));
+      }
+      if (routed >= 0.0) {
+        hw = true;
+        w = __dsub_rn(routed, arr);
+      }
+      pre += P.o_preempt[g];
+      tok += d;
+      tbtc += htb;
+      fa = arr < fa ? arr : fa;
+      lc = comp > lc ? comp : lc;
+    }
+    const unsigned cm = __ballot_sync(kFull, c), tm = __ballot_sync(kFull, htb),
+                   wm = __ballot_sync(kFull, hw);
+    // sequential sums in pool-index order (bit-identical to compute_metrics)
+    for (int k = 0; k < kWarp; ++k) {
+      const double ek = __shfl_sync(kFull, e, k), tk = __shfl_sync(kFull, t, k);
+      const double bk = __shfl_sync(kFull, tb, k), wk = __shfl_sync(kFull, w, k);
+      if ((cm >> k) & 1u) {
+        se = __dadd_rn(se, ek);
+        st = __dadd_rn(st, tk);
+      }
+      if ((tm >> k) & 1u) sb = __dadd_rn(sb, bk);
+      if ((wm >> k) & 1u) sw = __dadd_rn(sw, wk);
+    }
+  }
+  pre = warp_sum_ll(pre);
+  tok = warp_sum_ll(tok);
+  tbtc = warp_sum_ll(tbtc);
+  {
+    unsigned long long a = (unsigned long long)__double_as_longlong(fa);
+    a = warp_min_u64(a);  // non-negative doubles order like their bits
+    fa = __longlong_as_double((long long)a);
+    unsigned long long b = (unsigned long long)__double_as_longlong(lc);
+    b = warp_max_u64(b);
+    lc = __longlong_as_double((long long)b);
+  }
+  if (l == 0) {
+    rs_replay_stats s;
+    s.ticks = R.tick;
+    s.routed = R.routed;
+    s.infeasible = R.infeasible;
+    s.completed = R.completed;
+    s.decision_hash = R.hash;
+    s.sum_router_queue = R.sum_q;
+    s.sum_instance_waiting = R.sum_w;
+    s.total_preemptions = pre;
+    s.total_tokens = tok;
+    s.tbt_count = tbtc;
+    s.clock = R.clock;
+    s.total_e2e_s = se;
+    s.total_ttft_s = st;
+    s.total_tbt_s = sb;
+    s.total_router_wait_s = sw;
+    s.first_arrival_s = fa;
+    s.last_completion_s = lc;
+    s.makespan_s = __dsub_rn(lc, fa);
+    s.e2e_p50 = s.e2e_p90 = s.e2e_p99 = 0.0;
+    s.ttft_p50 = s.ttft_p90 = s.ttft_p99 = 0.0;
+    s.tbt_p50 = s.tbt_p90 = s.tbt_p99 = 0.0;
+    s.status = R.status;
+    s.error_instance = R.err_inst;
+    s.percentiles_valid = 0;
+    s._pad0 = 0;
+    s.injected = R.cursor;
+    for (int k = 0; k < 4; ++k) s._pad[k] = 0;
+    P.stats[r] = s;
+  }
+  __syncwarp();
+}
+
+template <int POL>
+__global__ void __launch_bounds__(256) replay_kernel(const __grid_constant__ KParams P) {
+  extern __shared__ __align__(16) char smem[];
+  const int w = threadIdx.x / kWarp;
+  MlpView M;
+  M.layers = P.rl_layers;
+  M.dims = P.rl_dims;
+  M.woff = P.rl_woff;
+  M.boff = P.rl_boff;
+  M.w = reinterpret_cast<const double*>(smem);
+  int groups_off = 0;
+  if (POL == RS_POLICY_RL) {
+    mlp_stage_weights(P.rl_w, P.rl_layers, P.rl_dims, P.rl_woff, P.rl_boff,
+                      reinterpret_cast<double*>(smem));
+    groups_off = P.smem_weights_bytes;
+  }
+  char* gbase = smem + groups_off + (size_t)w * P.smem_group_bytes;
+  const Grp G = make_grp(P, gbase);
+  for (;;) {
+    int r = 0;
+    if (lane_id() == 0) r = atomicAdd(P.work_counter, 1);
+    r = __shfl_sync(kFull, r, 0);
+    if (r >= P.num_replays) break;
+    run_replay<POL>(P, G, M, r);
+  }
+}
+
+}  // namespace rs

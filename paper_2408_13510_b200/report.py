@@ -1,0 +1,58 @@
+"""Per-replay report in the reference's summary.json shape (metrics.hpp:84-194).
+
+The fp64 sums are the engine's own sequential, pool-index-order sums
+(rs_replay_stats), so means are bit-identical to compute_metrics; the
+nearest-rank percentiles are taken here on the host from the per-request
+outputs (aggregate_of, metrics.hpp:62-80).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+
+def nearest_rank(sorted_values: np.ndarray, q: float) -> float:
+    n = sorted_values.shape[0]
+    idx = int(math.ceil(q * n))
+    if idx > 0:
+        idx -= 1
+    return float(sorted_values[min(idx, n - 1)])
+
+
+def _agg(values: np.ndarray, total: float) -> dict:
+    n = int(values.shape[0])
+    if n == 0:
+        return {"mean": 0.0, "p50": 0.0, "p90": 0.0, "p99": 0.0, "count": 0}
+    v = np.sort(values)
+    return {"mean": total / n, "p50": nearest_rank(v, 0.50), "p90": nearest_rank(v, 0.90),
+            "p99": nearest_rank(v, 0.99), "count": n}
+
+
+def summary(arrival, decode, routed, first, completion, preemptions, stats, num_instances) -> dict:
+    """report_to_json(compute_metrics(...)) for one replay (metrics.hpp:172-194)."""
+    done = completion >= 0.0
+    e2e = completion[done] - arrival[done]
+    ttft = first[done] - arrival[done]
+    dd = decode[done]
+    has_tbt = dd >= 2
+    tbt = (completion[done][has_tbt] - first[done][has_tbt]) / (dd[has_tbt] - 1).astype(np.float64)
+    ticks = int(stats["ticks"])
+    out = {
+        "completed": int(stats["completed"]),
+        "total_tokens": int(stats["total_tokens"]),
+        "total_e2e_s": float(stats["total_e2e_s"]),
+        "makespan_s": float(stats["makespan_s"]),
+        "e2e_s": _agg(e2e, float(stats["total_e2e_s"])),
+        "ttft_s": _agg(ttft, float(stats["total_ttft_s"])),
+        "tbt_s": _agg(tbt, float(stats["total_tbt_s"])),
+        "mean_router_wait_s": (float(stats["total_router_wait_s"]) / int(done.sum())
+                               if done.any() else 0.0),
+        "mean_router_queue": float(stats["sum_router_queue"]) / ticks if ticks else 0.0,
+        "mean_instance_waiting": (float(stats["sum_instance_waiting"]) / (ticks * num_instances)
+                                  if ticks else 0.0),
+        "mean_throughput_tokens_s": (float(stats["total_tokens"]) / float(stats["makespan_s"])
+                                     if float(stats["makespan_s"]) > 0.0 else 0.0),
+        "total_preemptions": int(stats["total_preemptions"]),
+    }
+    return out
