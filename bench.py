@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark: routing decisions/s over batched trace replays (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl engine|reference]
+
+Default workload (config c2 of BASELINE.json): 31,329-request 5-task-mix
+traces (Poisson lambda = 20/s), 1,024 seeds per GPU, 8 instances, the
+workload-aware router.  One step = one pass of the hot path over the whole
+batch: predictor kernel (d) + fused replay kernel (a+b+c) with the inputs
+resident in HBM, then a final NCCL all-gather of the per-replay statistics.
+
+ * value : decisions (ClusterSim ticks) of all replays of all ranks / max-over-
+           ranks device time of the step (CUDA events on the launch stream).
+ * e2e   : the same metric through the reference-facing C-ABI host call
+           rs_replay_batch_host with pinned host buffers (H2D + kernels + D2H
+           of every per-request result inside the timed region).
+ * cpu_baseline (rank 0, N = 1): the compiled UNMODIFIED reference
+           (oracle/_ref) on the host cores over a bounded seed sample.
+ * --impl reference: the reference's own CPU path on all host cores.
+Multi-GPU: one process per GPU (torchrun), replays sharded by seed (weak
+scaling, no data-path collective), stats gathered over NCCL at the end.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "routing decisions/sec over batched trace replays (whole box) at 1/2/4/8 B200"
+UNIT = "decisions/s"
+REPLAY_BYTES_PER_REQUEST = 8 + 4 + 4 + 1 + (4 + 8 + 8 + 8 + 4)  # in: arrival, prompt, decode, bucket; out
+REPLAY_BYTES_PER_REPLAY = 8 + 256  # offsets + stats record
+
+CONFIGS = {
+    # name: (requests, replays per GPU, instances, rate, policy, weights, description)
+    "c1": (2000, 1, 4, 20.0, "workload_aware", None,
+           "c1: single 2,000-request 5-task-mix trace (lambda=20), 4 instances, workload_aware"),
+    "c2": (31329, 1024, 8, 20.0, "workload_aware", None,
+           "c2: 31,329-request 5-task-mix trace (Poisson lambda=20) x 1,024 seeds per GPU, "
+           "8 instances, workload_aware router"),
+    "c3": (4000, 4096, 8, 40.0, "rl", None,
+           "c3: RL Q-network (51-64-64-9, random init seed 42) greedy rollouts, 4,096 replays x "
+           "4,000 requests (lambda=40), 8 instances"),
+    "c5": (200000, 512, 64, 40.0, "workload_aware", (0.0, 3.0, 1.0, 2.0, 0.0),
+           "c5: 64 instances, 200k-request heavy-decode mixture (weights 0/3/1/2/0, lambda=40) "
+           "x 512 seeds per GPU"),
+}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.out = b""
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for line in self.out.decode(errors="replace").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8 or not f[0].isdigit() or int(f[0]) not in self.gpus:
+                continue
+            try:
+                rows.append((int(f[1]), int(f[2]), f[4:8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        load = [r for r in rows if r[0] > 500] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[2]) if v == "Active"})
+        return {"sm_mhz": float(np.median([r[0] for r in load])),
+                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons, "samples": len(load)}
+
+
+def make_workload(cfgname, rank, threads=0):
+    from paper_2408_13510_b200 import abi, engine
+    n, R, m, rate, policy, weights, desc = CONFIGS[cfgname]
+    seeds = np.arange(rank * R + 1, rank * R + R + 1, dtype=np.uint64)
+    tb = engine.build_workload(seeds, n, rate, weights, threads=threads)
+    pseeds = np.array([abi.mix_seed(int(s), 0x9DED) for s in seeds], np.uint64)
+    return tb, pseeds, seeds
+
+
+def agent_for(m):
+    """DqnAgent(state_dim, m+1, hidden 64, seed 42) initial weights (Mlp::random)."""
+    from paper_2408_13510_b200 import abi, engine
+    sd = abi.state_dimension(m)
+    dims = [sd, 64, 64, m + 1]
+    return dims, engine.mlp_random_init(dims, 42)
+
+
+def cpu_reference(cfgname, sample_replays, threads):
+    """Compiled unmodified reference (oracle/_ref) on host threads."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracles as O  # baseline infrastructure
+    from paper_2408_13510_b200 import abi
+    n, R, m, rate, policy, weights, desc = CONFIGS[cfgname]
+    lib = O.ref_lib()
+    seeds = np.arange(1, sample_replays + 1, dtype=np.uint64)
+    from paper_2408_13510_b200 import engine
+    tb = engine.build_workload(seeds, n, rate, weights, threads=threads)
+    ps = np.array([abi.mix_seed(int(s), 0x9DED) for s in seeds], np.uint64)
+    cfg = abi.default_config(policy, m)
+    keep = None
+    if policy == "rl":
+        dims, params = agent_for(m)
+        keep = abi.set_rl(cfg, dims, params)
+    stats = np.zeros(sample_replays, abi.STATS_DTYPE)
+    wall = lib.ref_run_batch(C.byref(cfg), sample_replays, tb.offsets.ctypes.data,
+                             tb.arrival.ctypes.data, tb.prompt.ctypes.data, tb.decode.ctypes.data,
+                             tb.task.ctypes.data, ps.ctypes.data, None, threads,
+                             stats.ctypes.data)
+    del keep
+    if wall <= 0:
+        raise RuntimeError("reference batch failed: " + O.ref_error())
+    ticks = int(stats["ticks"].sum())
+    return ticks / wall, ticks, wall
+
+
+def run_reference_impl(args, cfgname):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n, R, m, rate, policy, weights, desc = CONFIGS[cfgname]
+    sample = threads
+    rates = []
+    for i in range(args.warmup + args.steps):
+        v, ticks, wall = cpu_reference(cfgname, sample, threads)
+        if i >= args.warmup:
+            rates.append((v, wall))
+    value = float(np.mean([r[0] for r in rates]))
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(np.mean([r[1] for r in rates]) * 1e3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference workload generator)",
+            "config": {"workload": desc, "policy": policy, "instances": m,
+                       "requests_per_replay": n},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{sample} replays (seeds 1..{sample}) of the {cfgname} "
+                                       f"workload, one per host thread, per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--replays", type=int, default=0, help="override replays per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.replays:
+        n, R, m, rate, pol, w, desc = CONFIGS[args.config]
+        CONFIGS[args.config] = (n, args.replays, m, rate, pol, w,
+                                desc.replace(f"{R:,}", f"{args.replays:,}"))
+    if args.impl == "reference":
+        run_reference_impl(args, args.config)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2408_13510_b200 import abi, engine
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = abi.load_library()
+    if lib.rs_device_count() < 1:
+        raise RuntimeError("no sm_100 device")
+    n, R, m, rate, policy, weights, desc = CONFIGS[args.config]
+    t_gen = time.time()
+    tb, pseeds, seeds = make_workload(args.config, rank)
+    t_gen = time.time() - t_gen
+    N = tb.total
+    dev = torch.device("cuda", local)
+    tt = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    d_off, d_arr, d_pr, d_de, d_tk = (tt(tb.offsets), tt(tb.arrival), tt(tb.prompt),
+                                      tt(tb.decode), tt(tb.task))
+    d_ps = tt(pseeds.view(np.int64))
+    o_in = torch.empty(N, dtype=torch.int32, device=dev)
+    o_ro = torch.empty(N, dtype=torch.float64, device=dev)
+    o_fi = torch.empty(N, dtype=torch.float64, device=dev)
+    o_co = torch.empty(N, dtype=torch.float64, device=dev)
+    o_pe = torch.empty(N, dtype=torch.int32, device=dev)
+    o_pb = torch.empty(N, dtype=torch.uint8, device=dev)
+    d_st = torch.zeros(R * 256, dtype=torch.uint8, device=dev)
+    cfg = abi.default_config(policy, m)
+    keep = None
+    if policy == "rl":
+        dims, params = agent_for(m)
+        d_params = tt(params)
+        keep = abi.set_rl(cfg, dims, params)  # host copy for the e2e call
+        dcfg = abi.BatchCfg.from_buffer_copy(bytes(cfg))
+        dcfg.rl_params = C.cast(C.c_void_p(d_params.data_ptr()), C.POINTER(C.c_double))
+    else:
+        dcfg = cfg
+    ws_bytes = C.c_size_t(0)
+    abi.check(lib, lib.rs_workspace_size(C.byref(dcfg), R, N, C.byref(ws_bytes)))
+    d_ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=dev)
+    tr = abi.TraceSoA(R, 0, N, d_off.data_ptr(), d_arr.data_ptr(), d_pr.data_ptr(),
+                      d_de.data_ptr(), d_tk.data_ptr(), None, d_ps.data_ptr(), None)
+    out = abi.ReqOut(o_in.data_ptr(), o_ro.data_ptr(), o_fi.data_ptr(), o_co.data_ptr(),
+                     o_pe.data_ptr(), o_pb.data_ptr())
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+    gathered = torch.empty(world * R * 256, dtype=torch.uint8, device=dev) if world > 1 else None
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        abi.check(lib, lib.rs_predict_buckets(C.byref(dcfg), C.byref(tr), o_pb.data_ptr(), sh))
+        if ev is not None:
+            ev[1].record(stream)
+        abi.check(lib, lib.rs_replay_batch(C.byref(dcfg), C.byref(tr), C.byref(out),
+                                           d_st.data_ptr(), d_ws.data_ptr(), ws_bytes.value, sh))
+        if ev is not None:
+            ev[2].record(stream)
+        if world > 1:  # final gather of the per-replay statistics (NCCL)
+            dist.all_gather_into_tensor(gathered, d_st)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    stats = np.frombuffer(d_st.cpu().numpy().tobytes(), dtype=abi.STATS_DTYPE)
+    ticks_local = int(stats["ticks"].sum())
+    unfinished = int((stats["status"] != abi.REPLAY_FINISHED).sum())
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(list(range(world)) if world > 1 else [local]) as clk:
+        start.record(stream)
+        for k in range(args.steps):
+            step(evs[k])
+        stop.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    elapsed = start.elapsed_time(stop) / 1e3
+    replay_s = sum(e[1].elapsed_time(e[2]) for e in evs) / 1e3 / args.steps
+    pred_s = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3 / args.steps
+    t = torch.tensor([elapsed, float(ticks_local)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = t.clone()
+        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm[1:], op=dist.ReduceOp.SUM)
+        elapsed, ticks_total = float(mx[0]), float(sm[1])
+    else:
+        ticks_total = float(ticks_local)
+    value = ticks_total * args.steps / elapsed
+
+    # ------------------------------------------------------------ e2e (C ABI)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        h_off, h_arr, h_pr, h_de, h_tk, h_ps = (pin(tb.offsets), pin(tb.arrival), pin(tb.prompt),
+                                                pin(tb.decode), pin(tb.task),
+                                                pin(pseeds.view(np.int64)))
+        hout = [torch.empty(N, dtype=d, pin_memory=True) for d in
+                (torch.int32, torch.float64, torch.float64, torch.float64, torch.int32,
+                 torch.uint8)]
+        h_st = torch.zeros(R * 256, dtype=torch.uint8, pin_memory=True)
+        htr = abi.TraceSoA(R, 0, N, h_off.data_ptr(), h_arr.data_ptr(), h_pr.data_ptr(),
+                           h_de.data_ptr(), h_tk.data_ptr(), None, h_ps.data_ptr(), None)
+        hro = abi.ReqOut(*[x.data_ptr() for x in hout])
+        h2d = 8 * (R + 1) + 8 * N + 4 * N + 4 * N + N + 8 * R
+        if policy == "rl":
+            h2d += 8 * abi.mlp_param_count(agent_for(m)[0])
+        d2h = N * (4 + 8 + 8 + 8 + 4 + 1) + 256 * R
+
+        def e2e_step():
+            abi.check(lib, lib.rs_replay_batch_host(C.byref(cfg), C.byref(htr), C.byref(hro),
+                                                    h_st.data_ptr(), local))
+        e2e_step()  # warm the arena
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": ticks_total * args.steps / float(te[0]), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(te[0]) * 1e3 / args.steps,
+               "path": "rs_replay_batch_host (C ABI, pinned host buffers)"}
+        h_stats = np.frombuffer(h_st.numpy().tobytes(), dtype=abi.STATS_DTYPE)
+        if not np.array_equal(h_stats["decision_hash"], stats["decision_hash"]):
+            raise RuntimeError("e2e path decisions differ from the device path")
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = load_peaks()
+    alg_bytes = REPLAY_BYTES_PER_REQUEST * N + REPLAY_BYTES_PER_REPLAY * R
+    achieved = alg_bytes / replay_s / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / f"ncu_replay_{args.config}.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except (ValueError, OSError):
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: reference workload generator, seeds 1..{R * world} "
+                f"(rank r takes seeds r*{R}+1..(r+1)*{R})",
+        "config": {"workload": desc, "policy": policy, "instances": m,
+                   "requests_per_replay": n, "replays_per_gpu": R, "arrival_rate": rate,
+                   "predictor": "simulated, Table-1 accuracy",
+                   "l2": f"inputs {(8 + 4 + 4 + 1) * N / 1e6:.0f} MB per GPU > 126 MB L2 "
+                         "(no flush needed)",
+                   "parallelism": f"replay shards x{world} (weak)"},
+        "decisions_per_step": ticks_total, "unfinished_replays": unfinished,
+        "gpu_launches": 2 * args.steps * world,
+        "kernel_ms": {"predict_buckets": pred_s * 1e3, "replay": replay_s * 1e3},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "rs::replay_kernel",
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "peak_source": peak_src},
+        "clocks": clk.summary(),
+        "trace_gen_s": t_gen,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            sample = min(threads, 64)
+            cv, cticks, cwall = cpu_reference(args.config if args.config != "c5" else "c5",
+                                              sample, threads)
+            line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": min(threads, sample),
+                                    "kind": "reference",
+                                    "sample": f"{sample} replays (seeds 1..{sample}) of the "
+                                              f"{args.config} workload on {min(threads, sample)} "
+                                              f"host threads, {cwall:.1f} s wall, "
+                                              f"{cticks} decisions"}
+        except Exception as e:  # baseline is reported, never the target
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    print(json.dumps(line), flush=True)
+    del keep
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

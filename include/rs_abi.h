@@ -304,6 +304,11 @@ rs_status rs_generate_mixture_batch(const rs_profile* profile,
                                     double* arrival_s, int32_t* prompt_tokens,
                                     int32_t* decode_tokens, uint8_t* task);
 
+/* Mlp::random (mlp.hpp:32-45) as DqnAgent's constructor uses it
+ * (dqn.hpp:60-65): Rng(seed), w = (2u - 1) * sqrt(2 / fan_in), b = 0. */
+rs_status rs_mlp_random_init(const int32_t* dims, int32_t num_layers, uint64_t seed,
+                             double* params_out);
+
 /* mix_seed (rng.hpp:11-16). */
 uint64_t rs_mix_seed(uint64_t seed, uint64_t stream);
 

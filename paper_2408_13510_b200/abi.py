@@ -282,7 +282,7 @@ EXPORTED_SYMBOLS = (
     "rs_validate_config", "rs_workspace_size", "rs_predict_buckets",
     "rs_replay_batch", "rs_replay_batch_host", "rs_mlp_forward_host",
     "rs_generate_mixture", "rs_generate_mixture_batch", "rs_mix_seed",
-    "rs_heavy_decode_cutoff", "rs_host_alloc", "rs_host_free",
+    "rs_heavy_decode_cutoff", "rs_host_alloc", "rs_host_free", "rs_mlp_random_init",
 )
 
 
@@ -312,6 +312,7 @@ def _declare(lib: C.CDLL) -> None:
     lib.rs_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
     lib.rs_heavy_decode_cutoff.restype = C.c_int64
     lib.rs_heavy_decode_cutoff.argtypes = [P(Profile), P(Thresholds)]
+    lib.rs_mlp_random_init.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p]
     lib.rs_host_alloc.restype = C.c_void_p
     lib.rs_host_alloc.argtypes = [C.c_size_t]
     lib.rs_host_free.argtypes = [C.c_void_p]

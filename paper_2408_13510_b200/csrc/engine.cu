@@ -18,6 +18,7 @@
 #include "mlp.cuh"
 #include "predictor.cuh"
 #include "router.cuh"
+#include "fast_kernel.cuh"
 
 namespace {
 
@@ -76,15 +77,18 @@ int min_reservation(const rs_batch_cfg& c) {
   return (int)std::max<int64_t>(2, 1 + mn);
 }
 
-Layout make_layout(const rs_batch_cfg& c, int wcap) {
+// fast = the lane-per-instance kernel (no InstHot block, 5 running fields
+// with an odd per-instance stride so lane-owned rows hit distinct banks).
+Layout make_layout(const rs_batch_cfg& c, int wcap, bool fast) {
   Layout L{};
   const int m = c.num_instances;
   L.rcap = (int)std::min<int64_t>(c.max_batch_size, c.kv_capacity_tokens / min_reservation(c));
   if (L.rcap < 1) L.rcap = 1;
   L.wcap = wcap;
-  size_t off = (size_t)m * sizeof(rs::InstHot);
+  size_t off = fast ? 0 : (size_t)m * sizeof(rs::InstHot);
   L.off_run = (int)off;
-  off = align_up(off + 6ull * m * L.rcap * sizeof(int), 16);
+  off = fast ? align_up(off + 5ull * m * (L.rcap | 1) * sizeof(int), 16)
+             : align_up(off + 6ull * m * L.rcap * sizeof(int), 16);
   L.off_wait = (int)off;
   off = align_up(off + 5ull * m * L.wcap * sizeof(int), 16);
   L.off_dbc = (int)off;
@@ -223,10 +227,9 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-template <int POL>
-rs_status launch_replay(const rs::KParams& kp, int wpb, int block_smem, int num_replays,
+template <typename K>
+rs_status launch_kernel(K kern, const rs::KParams& kp, int wpb, int block_smem, int num_replays,
                         cudaStream_t st) {
-  auto kern = rs::replay_kernel<POL>;
   RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, block_smem));
   int dev = 0, sms = 0, per_sm = 0;
   RS_CUDA(cudaGetDevice(&dev));
@@ -238,6 +241,42 @@ rs_status launch_replay(const rs::KParams& kp, int wpb, int block_smem, int num_
   kern<<<grid, wpb * rs::kWarp, block_smem, st>>>(kp);
   RS_CUDA(cudaGetLastError());
   return RS_OK;
+}
+
+using KernelFn = void (*)(rs::KParams);
+
+}  // namespace
+
+// One translation unit per policy (generated by build.py, compiled in
+// parallel) instantiates that policy's general and fast replay kernels.
+namespace rs {
+using KernelFn = void (*)(KParams);
+KernelFn kernel_for_0(bool fast, int groups);
+KernelFn kernel_for_1(bool fast, int groups);
+KernelFn kernel_for_2(bool fast, int groups);
+KernelFn kernel_for_3(bool fast, int groups);
+KernelFn kernel_for_4(bool fast, int groups);
+KernelFn kernel_for_5(bool fast, int groups);
+KernelFn kernel_for_6(bool fast, int groups);
+KernelFn kernel_for_7(bool fast, int groups);
+KernelFn kernel_for_8(bool fast, int groups);
+}  // namespace rs
+
+namespace {
+
+KernelFn kernel_for(int policy, bool fast, int groups) {
+  switch (policy) {
+    case 0: return rs::kernel_for_0(fast, groups);
+    case 1: return rs::kernel_for_1(fast, groups);
+    case 2: return rs::kernel_for_2(fast, groups);
+    case 3: return rs::kernel_for_3(fast, groups);
+    case 4: return rs::kernel_for_4(fast, groups);
+    case 5: return rs::kernel_for_5(fast, groups);
+    case 6: return rs::kernel_for_6(fast, groups);
+    case 7: return rs::kernel_for_7(fast, groups);
+    case 8: return rs::kernel_for_8(fast, groups);
+  }
+  return nullptr;
 }
 
 }  // namespace
@@ -395,7 +434,10 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
   char* ws = static_cast<char*>(workspace);
 
   const int wcap = std::max(8, std::min(128, env_int("RS_WAIT_RING", 64)));
-  Layout L = make_layout(*cfg, wcap);
+  // whole-prompt prefill (no chunking) takes the lane-per-instance kernel
+  const bool fast = cfg->chunk_size == 0 && env_int("RS_FORCE_GENERAL", 0) == 0;
+  const int groups = cfg->num_instances <= 32 ? 1 : (cfg->num_instances <= 64 ? 2 : 4);
+  Layout L = make_layout(*cfg, wcap, fast);
   rs::KParams kp;
   std::memset(&kp, 0, sizeof(kp));
   const rs_profile& p = cfg->profile;
@@ -492,17 +534,8 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
                                         std::to_string(L.weights_bytes + L.group_bytes) + " B)");
   const int block_smem = L.weights_bytes + best_wpb * L.group_bytes;
   RS_CUDA(cudaMemsetAsync(kp.work_counter, 0, sizeof(int), st));
-  switch (cfg->policy) {
-    case RS_POLICY_ROUND_ROBIN: return launch_replay<RS_POLICY_ROUND_ROBIN>(kp, best_wpb, block_smem, tr->num_replays, st);
-    case RS_POLICY_DEDICATED_SMALL_LARGE: return launch_replay<RS_POLICY_DEDICATED_SMALL_LARGE>(kp, best_wpb, block_smem, tr->num_replays, st);
-    case RS_POLICY_DECODE_BALANCER: return launch_replay<RS_POLICY_DECODE_BALANCER>(kp, best_wpb, block_smem, tr->num_replays, st);
-    case RS_POLICY_JSQ: return launch_replay<RS_POLICY_JSQ>(kp, best_wpb, block_smem, tr->num_replays, st);
-    case RS_POLICY_MAX_CAPACITY: return launch_replay<RS_POLICY_MAX_CAPACITY>(kp, best_wpb, block_smem, tr->num_replays, st);
-    case RS_POLICY_MIN_MIN: return launch_replay<RS_POLICY_MIN_MIN>(kp, best_wpb, block_smem, tr->num_replays, st);
-    case RS_POLICY_EARLIEST_AVAILABLE: return launch_replay<RS_POLICY_EARLIEST_AVAILABLE>(kp, best_wpb, block_smem, tr->num_replays, st);
-    case RS_POLICY_WORKLOAD_AWARE: return launch_replay<RS_POLICY_WORKLOAD_AWARE>(kp, best_wpb, block_smem, tr->num_replays, st);
-    case RS_POLICY_RL: return launch_replay<RS_POLICY_RL>(kp, best_wpb, block_smem, tr->num_replays, st);
-  }
+  KernelFn kern = kernel_for(cfg->policy, fast, groups);
+  if (kern) return launch_kernel(kern, kp, best_wpb, block_smem, tr->num_replays, st);
   return fail(RS_ERR_INVALID_ARGUMENT, "unknown policy");
 }
 

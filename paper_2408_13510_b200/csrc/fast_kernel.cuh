@@ -1,0 +1,428 @@
+// fast_kernel.cuh — tick loop of the fast (lane = instance) replay kernel.
+#pragma once
+
+#include "fast.cuh"
+
+namespace rs {
+
+// InstanceFeatures (instance.hpp:317-360) of the lane's instance at a tick
+// boundary, from the maintained aggregates.  At a step boundary every
+// admitted prompt has been prefilled, so running prompt-bucket counts and
+// pending running prompt tokens are zero.
+__device__ __forceinline__ Feat feat_of(const Inst& I) {
+  Feat f;
+  f.res = I.res + I.resw;
+  f.pend = I.pend + I.pendw;
+  f.dleft = I.dleft + I.dlw;
+  f.tleft = I.tleft + I.tlw;
+  f.tok = I.tok + I.tokw;
+  f.cnt = I.n + I.w_cnt + I.o_cnt;
+  f.kv = I.kv;
+  f.nrun = I.n;
+  f.mind = I.n == 0 ? 0 : (I.nge > 0 ? 0 : I.next_ge - I.D);
+  return f;
+}
+
+// decode-bucket counts (state edges) of instance i's running batch
+__device__ inline void warp_dbc(const KParams& P, const FastGrp& G, int i, int owner,
+                                const Inst& I, int* dbc) {
+  const int l = lane_id();
+  const int D = __shfl_sync(kFull, I.D, owner);
+  const int n = __shfl_sync(kFull, I.n, owner);
+  const int base = i * G.R.stride;
+  int cnt[RS_MAX_BUCKETS];
+#pragma unroll
+  for (int b = 0; b < RS_MAX_BUCKETS; ++b) cnt[b] = 0;
+  for (int j = l; j < n; j += kWarp) {
+    const int d = G.R.dhat[base + j] - (D + G.R.key[base + j]);
+    cnt[bucket_of(P.state_edges, P.n_state_edges, d > 0 ? d : 0)]++;
+  }
+#pragma unroll
+  for (int b = 0; b < RS_MAX_BUCKETS; ++b) {
+    const int c = warp_sum(cnt[b]);
+    if (l == b) dbc[i * RS_MAX_BUCKETS + b] = c;
+  }
+}
+
+template <int POL, int G>
+__device__ inline int decide_fast(const KParams& P, const FastGrp& FG, const MlpView& M,
+                                  Replay& R, const Inst (&S)[G], bool has_head, const Rec& hr,
+                                  int hb, int* dbc) {
+  const int m = P.m;
+  const int l = lane_id();
+  const int need = reserved_of(hr.prompt, hr.dhat, 0);
+  if (POL == RS_POLICY_ROUND_ROBIN || POL == RS_POLICY_DEDICATED_SMALL_LARGE) {
+    if (!has_head) return m;
+    int t;
+    if (POL == RS_POLICY_ROUND_ROBIN) {
+      t = (int)(R.rr_next % (unsigned long long)m);
+    } else {
+      if (m < 2 || hr.dhat >= P.dsl_cutoff) t = 0;
+      else t = 1 + (int)(R.dsl_next % (unsigned long long)(m - 1));
+    }
+    bool ok = false;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (g * kWarp + l == t) ok = can_accept(P, feat_of(S[g]), need);
+    ok = __shfl_sync(kFull, ok, t & (kWarp - 1));
+    if (!ok) return m;
+    if (POL == RS_POLICY_ROUND_ROBIN) R.rr_next++;
+    else if (m >= 2 && t >= 1) R.dsl_next++;
+    return t;
+  } else if (POL == RS_POLICY_EARLIEST_AVAILABLE) {
+    if (!has_head) return m;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int i = g * kWarp + l;
+      const bool ok = i < m && (long long)P.kv_cap - feat_of(S[g]).res >= need;
+      const unsigned b = __ballot_sync(kFull, ok);
+      if (b) return g * kWarp + __ffs(b) - 1;
+    }
+    return m;
+  } else if (POL == RS_POLICY_MAX_CAPACITY) {
+    if (!has_head || R.clock < R.mc_next) return m;
+    unsigned long long bk = 0;
+    int bi = -1;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int i = g * kWarp + l;
+      const bool v = i < m;
+      const unsigned long long k = v ? ordered_key(capacity_of(P, S[g].kv)) : 0ull;
+      const int a = warp_argmax_key(k, v);
+      if (a >= 0) {
+        const unsigned long long ka = __shfl_sync(kFull, k, a);
+        if (bi < 0 || ka > bk) { bk = ka; bi = g * kWarp + a; }
+      }
+    }
+    bool ok = false;
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (g * kWarp + l == bi) ok = (long long)P.kv_cap - feat_of(S[g]).res >= need;
+    ok = __shfl_sync(kFull, ok, bi & (kWarp - 1));
+    if (!ok) return m;
+    R.mc_next = __dadd_rn(R.clock, 1.0);
+    return bi;
+  } else if (POL == RS_POLICY_RL) {
+    double* x = FG.rlx;
+    const int nsb = P.n_state_edges;
+    const int per = 3 + nsb;
+    for (int i = 0; i < m; ++i) {  // decode-bucket counts, whole warp per instance
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if (i / kWarp == g) warp_dbc(P, FG, i, i & (kWarp - 1), S[g], dbc);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int i = g * kWarp + l;
+      if (i < m) {
+        const Feat f = feat_of(S[g]);
+        double* xi = x + i * per;
+        xi[0] = __ddiv_rn((double)f.pend, (double)P.kv_cap);
+        for (int b = 0; b < nsb; ++b)
+          xi[1 + b] = __ddiv_rn((double)dbc[i * RS_MAX_BUCKETS + b], (double)P.max_batch);
+        xi[1 + nsb] = round2(capacity_of(P, f.kv));
+        const double that = f.nrun == 0 ? 0.0 : __dmul_rn(P.dtb, (double)f.mind);
+        xi[2 + nsb] = round2(that);
+      }
+    }
+    if (l == 0) {
+      const int q = queue_len<POL>(R);
+      x[m * per] = __ddiv_rn((double)(q < 512 ? q : 512), 512.0);
+      x[m * per + 1] = has_head ? __ddiv_rn((double)hr.prompt, 1024.0) : 0.0;
+      x[m * per + 2] = has_head ? (double)hb : 0.0;
+    }
+    __syncwarp();
+    const int na = P.rl_dims[P.rl_layers];
+    if (P.rl_eps > 0.0) {
+      const double u = u01(rng_draw(FG.rng, R));
+      if (u < P.rl_eps) {
+        const double v = __dmul_rn(u01(rng_draw(FG.rng, R)), (double)na);
+        const unsigned long long k = (unsigned long long)v;
+        return (int)(k < (unsigned long long)na ? k : (unsigned long long)na - 1);
+      }
+    }
+    double* h0 = x + M.dims[0];
+    double* h1 = h0 + P.rl_maxw;
+    return mlp_forward_warp(M, x, h0, h1, nullptr);
+  } else {
+    if (!has_head) return m;
+    unsigned long long bk = ~0ull;
+    int bi = -1;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int i = g * kWarp + l;
+      bool v = i < m;
+      unsigned long long k = ~0ull;
+      if (v) {
+        const Feat f = feat_of(S[g]);
+        if (POL == RS_POLICY_DECODE_BALANCER) {  // policies.hpp:108-127
+          v = can_accept(P, f, need);
+          k = (unsigned long long)f.tleft;
+        } else if (POL == RS_POLICY_JSQ) {  // policies.hpp:131-146
+          k = (unsigned long long)(f.pend + f.dleft);
+        } else if (POL == RS_POLICY_MIN_MIN) {  // policies.hpp:193-206
+          k = ordered_key(__dadd_rn(__dmul_rn((double)f.pend, P.tpp),
+                                    __dmul_rn((double)f.dleft, P.dtb)));
+        } else {  // workload_aware, SURVEY.md Appendix B
+          v = can_accept(P, f, need);
+          const long long p = hr.prompt, d = hr.dhat;
+          const double avail = __dmul_rn(P.dtb, (double)f.dleft);
+          const double pcost = __dmul_rn(P.tpp, (double)(f.pend + p));
+          const double pi = (double)p;
+          const double lead = P.prompt_exp == 2 ? __dmul_rn(pi, pi) : pi;
+          const double t_p = __dmul_rn(P.grad1, __dadd_rn(lead, (double)f.tok));
+          const double r_p = t_p <= P.eps_s ? 1.0 : __dsub_rn(1.0, __ddiv_rn(t_p, P.eps_s));
+          const double r_d = __dmul_rn(-P.grad2, (double)(f.tok + p + d));
+          const double mix = __dadd_rn(__dmul_rn(P.alpha, r_p),
+                                       __dmul_rn(__dsub_rn(1.0, P.alpha), r_d));
+          k = ordered_key(__dsub_rn(__dadd_rn(avail, pcost), __dmul_rn(P.eps_s, mix)));
+        }
+      }
+      const int a = warp_argmin_key(k, v);
+      if (a >= 0) {
+        const unsigned long long ka = __shfl_sync(kFull, k, a);
+        if (bi < 0 || ka < bk) { bk = ka; bi = g * kWarp + a; }
+      }
+    }
+    if (POL == RS_POLICY_JSQ || POL == RS_POLICY_MIN_MIN) return bi;
+    return bi < 0 ? m : bi;
+  }
+}
+
+// Returns true when the replay must be re-run instance-sequentially.
+template <int POL, int G>
+__device__ bool run_replay_fast(const KParams& P, const FastGrp& FG, const MlpView& M, int r,
+                                bool seq, int* dbc) {
+  const int l = lane_id();
+  Replay R;
+  R.off = P.offsets[r];
+  R.n = (int)(P.offsets[r + 1] - R.off);
+  const int m = P.m;
+  const long long off = R.off;
+
+  bool bad = false;
+  for (int j = l; j < R.n; j += kWarp) {
+    const long long g = off + j;
+    P.o_instance[g] = -1;
+    P.o_routed[g] = -1.0;
+    P.o_first[g] = -1.0;
+    P.o_completion[g] = -1.0;
+    P.o_preempt[g] = 0;
+    if (POL == RS_POLICY_MIN_MIN) P.mm_removed[g] = 0;
+    const int p = P.prompt[g], d = P.decode[g];
+    if (p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens) bad = true;
+    if (j > 0 && P.arrival[g] < P.arrival[g - 1]) bad = true;
+  }
+  bad = __any_sync(kFull, bad);
+  Inst S[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) inst_init(S[g]);
+  R.clock = 0.0;
+  R.tick = 0;
+  R.qhead = R.cursor = 0;
+  R.completed = 0;
+  R.nfront = R.n_removed = 0;
+  R.total_wait = 0;
+  R.rr_next = R.dsl_next = 0;
+  R.mc_next = 0.0;
+  R.hash = 0xcbf29ce484222325ull;
+  R.infeasible = R.routed = R.sum_q = R.sum_w = 0;
+  R.status = RS_REPLAY_FINISHED;
+  R.err_inst = -1;
+  R.rng_pos = 312;
+  R.a_base = 0;
+  R.h_base = -2 * kWarp;
+  R.h_prompt = R.h_true = R.h_bucket = 0;
+  if (POL == RS_POLICY_RL && P.rl_eps > 0.0)
+    mt_seed_warp(FG.rng, P.policy_seed ? P.policy_seed[r] : 0ull);
+  __syncwarp();
+  load_arrival_window(P, R);
+  if (bad) R.status = RS_REPLAY_INVALID_TRACE;
+  else inject(P, R);
+
+  while (R.status == RS_REPLAY_FINISHED && R.completed != R.n && R.tick < P.max_ticks) {
+    if (POL == RS_POLICY_MIN_MIN && queue_len<POL>(R) > 0) {
+      if (!minmin_pick(P, FG.front, R)) { R.status = RS_REPLAY_CAPACITY; break; }
+    }
+    const bool has_head = queue_len<POL>(R) > 0;
+    Rec hr;
+    int hb = 0;
+    if (has_head) hr = head_rec<POL>(P, FG.front, R, &hb);
+    else hr.req = hr.prompt = hr.dhat = hr.tru = hr.emit = 0;
+    const int action = decide_fast<POL, G>(P, FG, M, R, S, has_head, hr, hb, dbc);
+    R.hash = hash_action(R.hash, action);
+    if (action < 0 || action > m) { R.status = RS_REPLAY_BAD_ACTION; break; }
+    const double t1 = __dadd_rn(R.clock, P.delta_t);
+    if (action < m && has_head) {
+      if ((long long)hr.prompt + hr.tru > P.kv_cap) {
+        R.infeasible++;
+      } else {
+        if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) {
+          if (l == 0)
+            for (int k = 0; k + 1 < R.nfront; ++k) FG.front[k] = FG.front[k + 1];
+          __syncwarp();
+          R.nfront--;
+        } else {
+          R.qhead++;
+          if (POL == RS_POLICY_MIN_MIN) mm_skip_removed(P, R);
+        }
+        if (l == 0) {
+          P.o_routed[off + hr.req] = R.clock;
+          P.o_instance[off + hr.req] = action;
+        }
+        R.routed++;
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+          if (g * kWarp + l == action) lane_enqueue(P, FG, off, action, S[g], hr, R.clock);
+      }
+    }
+
+    // ---- run_until(t1) for every instance (env.hpp:277-287) -----------
+    int err = kBig;
+    for (;;) {
+      bool act[G];
+      unsigned any = 0;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int i = g * kWarp + l;
+        act[g] = false;
+        if (i < m && S[g].clock < t1) {
+          if (S[g].n > 0 || S[g].w_cnt > 0) act[g] = true;
+          else S[g].clock = t1;  // idle instance skips ahead (instance.hpp:309)
+        }
+        any |= __ballot_sync(kFull, act[g]) ? (1u << g) : 0u;
+      }
+      if (!any) break;
+      if (seq) {  // only the lowest-index instance that still has work
+        const int g0 = __ffs(any) - 1;
+        const unsigned lm = __ballot_sync(kFull, act[g0 < G ? g0 : 0]);
+#pragma unroll
+        for (int g = 0; g < G; ++g) act[g] = act[g] && g == g0 && l == __ffs(lm) - 1;
+      }
+      bool first[G], dec[G], scan[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        first[g] = dec[g] = scan[g] = false;
+        if (!act[g]) continue;
+        Inst& I = S[g];
+        const int i = g * kWarp + l;
+        if (I.w_cnt > 0 && I.n < P.max_batch) lane_admit(P, FG, off, i, I);
+        if (I.n == 0) {  // logic_error, instance.hpp:209-211
+          err = min(err, i);
+          act[g] = false;
+          continue;
+        }
+        if (I.npf > 0) {  // whole-prompt prefill, co-running decodes stall
+          I.clock = __dadd_rn(I.clock, __dadd_rn(__dadd_rn(P.intercept, __dmul_rn(P.tpp, (double)I.pend)),
+                                                 __dmul_rn(P.dpt, (double)I.kv)));
+          I.kv += I.pend;
+          I.pend = 0;
+          I.npf = 0;
+        } else {  // every running request emits one token
+          const int n = I.n;
+          I.clock = __dadd_rn(I.clock, __dadd_rn(P.dtb, __dmul_rn(P.dpt, (double)n)));
+          I.D++;
+          I.kv += n;
+          I.tleft -= n;
+          I.tok += n;
+          I.res += I.nge;
+          I.dleft -= n - I.nge;
+          dec[g] = true;
+          first[g] = I.ft < n;
+          scan[g] = I.D >= I.next_done || I.D >= I.next_ge;
+        }
+      }
+      if (__any_sync(kFull, err != kBig)) {
+        err = warp_min(err);
+        if (!seq) return true;  // exact stop point needs index order: re-run
+        R.status = RS_REPLAY_NOT_ADMISSIBLE;
+        R.err_inst = err;
+        break;
+      }
+      // first tokens of the requests admitted since the last decode step
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (!first[g]) continue;
+        const Inst& I = S[g];
+        const int base = (g * kWarp + l) * FG.R.stride;
+        for (int j = I.ft; j < I.n; ++j) {
+          const int q = FG.R.req[base + j];
+          if (q & kFresh) P.o_first[off + (q & kReqMask)] = I.clock;
+        }
+      }
+      // completion / estimate-reached events: whole warp per instance
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        unsigned sm = __ballot_sync(kFull, scan[g]);
+        while (sm) {
+          const int owner = __ffs(sm) - 1;
+          sm &= sm - 1;
+          warp_scan_instance<false>(P, FG, off, g * kWarp + owner, owner, S[g], dbc);
+        }
+        if (dec[g]) S[g].ft = S[g].n;
+      }
+      // preemption (rare): owner lane evicts, whole warp rescans
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        bool pre = false;
+        if (act[g] && S[g].kv > P.kv_cap && S[g].n > 1)
+          pre = lane_preempt(P, FG, off, g * kWarp + l, S[g]);
+        unsigned pm = __ballot_sync(kFull, pre);
+        while (pm) {
+          const int owner = __ffs(pm) - 1;
+          pm &= pm - 1;
+          warp_scan_instance<false>(P, FG, off, g * kWarp + owner, owner, S[g], dbc);
+        }
+      }
+    }
+    if (R.status != RS_REPLAY_FINISHED) break;
+    int comps = 0, wait = 0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      comps += S[g].comps;
+      S[g].comps = 0;
+      if (g * kWarp + l < m) wait += S[g].w_cnt + S[g].o_cnt;
+    }
+    R.completed += warp_sum(comps);
+    R.clock = t1;
+    inject(P, R);
+    R.tick++;
+    R.sum_q += queue_len<POL>(R);
+    R.sum_w += warp_sum(wait);
+  }
+  if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
+  write_replay_stats(P, R, r);
+  return false;
+}
+
+template <int POL, int G>
+__global__ void __launch_bounds__(256) replay_fast_kernel(const __grid_constant__ KParams P) {
+  extern __shared__ __align__(16) char smem[];
+  const int w = threadIdx.x / kWarp;
+  MlpView M;
+  M.layers = P.rl_layers;
+  M.dims = P.rl_dims;
+  M.woff = P.rl_woff;
+  M.boff = P.rl_boff;
+  M.w = reinterpret_cast<const double*>(smem);
+  int groups_off = 0;
+  if (POL == RS_POLICY_RL) {
+    mlp_stage_weights(P.rl_w, P.rl_layers, P.rl_dims, P.rl_woff, P.rl_boff,
+                      reinterpret_cast<double*>(smem));
+    groups_off = P.smem_weights_bytes;
+  }
+  char* gbase = smem + groups_off + (size_t)w * P.smem_group_bytes;
+  const FastGrp FG = make_fast_grp(P, gbase);
+  int* dbc = reinterpret_cast<int*>(gbase + P.off_dbc);
+  for (;;) {
+    int r = 0;
+    if (lane_id() == 0) r = atomicAdd(P.work_counter, 1);
+    r = __shfl_sync(kFull, r, 0);
+    if (r >= P.num_replays) break;
+    if (run_replay_fast<POL, G>(P, FG, M, r, false, dbc))
+      run_replay_fast<POL, G>(P, FG, M, r, true, dbc);
+  }
+}
+
+}  // namespace rs

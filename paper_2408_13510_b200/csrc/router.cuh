@@ -80,8 +80,8 @@ __device__ __forceinline__ Rec load_req(const KParams& P, long long off, int req
 }
 
 template <int POL>
-__device__ __forceinline__ Rec head_rec(const KParams& P, const Grp& G, Replay& R, int* bucket) {
-  if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) return load_req(P, R.off, G.front[0], bucket);
+__device__ __forceinline__ Rec head_rec(const KParams& P, int* front, Replay& R, int* bucket) {
+  if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) return load_req(P, R.off, front[0], bucket);
   head_window(P, R, R.qhead);
   const int s = R.qhead - R.h_base;
   Rec r;
@@ -136,14 +136,14 @@ __device__ __forceinline__ void mm_skip_removed(const KParams& P, Replay& R) {
 // MinMinPolicy::pick_queue_index (policies.hpp:179-191) + move_to_front
 // (env.hpp:234-243).  Queue order = front list, then the range in index
 // order minus removed entries.  Returns false on front-list overflow.
-__device__ inline bool minmin_pick(const KParams& P, const Grp& G, Replay& R) {
+__device__ inline bool minmin_pick(const KParams& P, int* front, Replay& R) {
   const int l = lane_id();
   unsigned long long fk = ~0ull;
   int fpos = 0x7fffffff;
   if (R.nfront > 0) {
     unsigned long long k = ~0ull;
     if (l < R.nfront) {
-      const int req = G.front[l];
+      const int req = front[l];
       const double est = __dadd_rn(__dmul_rn(P.tpp, (double)P.prompt[R.off + req]),
                                    __dmul_rn(P.dtb, (double)P.ub[P.bucket[R.off + req]]));
       k = ordered_key(est);
@@ -172,11 +172,11 @@ __device__ inline bool minmin_pick(const KParams& P, const Grp& G, Replay& R) {
   }
   if (R.nfront > 0 && fk <= rk) {  // front entry (earlier queue positions win ties)
     if (fpos == 0) return true;
-    const int v = G.front[fpos];
+    const int v = front[fpos];
     __syncwarp();
     if (l == 0) {
-      for (int k = fpos; k > 0; --k) G.front[k] = G.front[k - 1];
-      G.front[0] = v;
+      for (int k = fpos; k > 0; --k) front[k] = front[k - 1];
+      front[0] = v;
     }
     __syncwarp();
     return true;
@@ -186,8 +186,8 @@ __device__ inline bool minmin_pick(const KParams& P, const Grp& G, Replay& R) {
   if (R.nfront >= kMaxFront) return false;
   if (l == 0) {
     P.mm_removed[R.off + ridx] = 1;
-    for (int k = R.nfront; k > 0; --k) G.front[k] = G.front[k - 1];
-    G.front[0] = ridx;
+    for (int k = R.nfront; k > 0; --k) front[k] = front[k - 1];
+    front[0] = ridx;
   }
   __syncwarp();
   R.nfront++;
@@ -197,9 +197,9 @@ __device__ inline bool minmin_pick(const KParams& P, const Grp& G, Replay& R) {
 }
 
 // ε-greedy stream (DqnAgent::act, dqn.hpp:92-99) in shared memory.
-__device__ __forceinline__ unsigned long long rng_draw(const Grp& G, Replay& R) {
-  unsigned long long* st = G.rng;
-  unsigned long long* ob = G.rng + 312;
+__device__ __forceinline__ unsigned long long rng_draw(unsigned long long* rngbuf, Replay& R) {
+  unsigned long long* st = rngbuf;
+  unsigned long long* ob = rngbuf + 312;
   if (R.rng_pos == 312) {
     mt_twist_warp(st);
     for (int k = lane_id(); k < 312; k += kWarp) ob[k] = mt_temper(st[k]);
@@ -282,9 +282,9 @@ __device__ inline int decide(const KParams& P, const Grp& G, const MlpView& M, R
     __syncwarp();
     const int na = P.rl_dims[P.rl_layers];
     if (P.rl_eps > 0.0) {
-      const double u = u01(rng_draw(G, R));
+      const double u = u01(rng_draw(G.rng, R));
       if (u < P.rl_eps) {
-        const double v = __dmul_rn(u01(rng_draw(G, R)), (double)na);
+        const double v = __dmul_rn(u01(rng_draw(G.rng, R)), (double)na);
         const unsigned long long k = (unsigned long long)v;  // static_cast<uint64_t>
         return (int)(k < (unsigned long long)na ? k : (unsigned long long)na - 1);
       }
@@ -338,157 +338,10 @@ __device__ inline int decide(const KParams& P, const Grp& G, const MlpView& M, R
   }
 }
 
-template <int POL>
-__device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int r) {
-  constexpr bool NEED_DBC = POL == RS_POLICY_RL;
+// Per-replay statistics (compute_metrics, metrics.hpp:84-162): fp64 sums are
+// sequential in pool-index order, bit-identical to the reference.
+__device__ inline void write_replay_stats(const KParams& P, const Replay& R, int r) {
   const int l = lane_id();
-  Replay R;
-  R.off = P.offsets[r];
-  R.n = (int)(P.offsets[r + 1] - R.off);
-  const int m = P.m;
-
-  // outputs to the reference's "not yet" values; input checks
-  bool bad = false;
-  for (int j = l; j < R.n; j += kWarp) {
-    const long long g = R.off + j;
-    P.o_instance[g] = -1;
-    P.o_routed[g] = -1.0;
-    P.o_first[g] = -1.0;
-    P.o_completion[g] = -1.0;
-    P.o_preempt[g] = 0;
-    if (POL == RS_POLICY_MIN_MIN) P.mm_removed[g] = 0;
-    const int p = P.prompt[g], d = P.decode[g];
-    if (p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens) bad = true;
-    if (j > 0 && P.arrival[g] < P.arrival[g - 1]) bad = true;
-  }
-  bad = __any_sync(kFull, bad);
-  for (int i = l; i < m; i += kWarp) {
-    InstHot h;
-    h.clock = 0.0;
-    h.res_wait = h.pend_wait = h.dleft_wait = h.tleft_wait = h.tok_wait = 0;
-    h.n_run = h.n_prefill = h.res_run = h.kv_run = h.pend_run = 0;
-    h.dleft_run = h.tleft_run = h.tok_run = 0;
-    h.min_dleft = 0x7fffffff;
-    h.w_head = h.w_cnt = h.o_cnt = 0;
-    h.o_head = h.o_tail = (int)kNil;
-    h._pad0 = h._pad1 = 0;
-    G.inst[i] = h;
-    if (NEED_DBC)
-      for (int b = 0; b < RS_MAX_BUCKETS; ++b) G.dbc[i * RS_MAX_BUCKETS + b] = 0;
-  }
-  R.clock = 0.0;
-  R.tick = 0;
-  R.qhead = R.cursor = 0;
-  R.completed = 0;
-  R.nfront = R.n_removed = 0;
-  R.total_wait = 0;
-  R.rr_next = R.dsl_next = 0;
-  R.mc_next = 0.0;
-  R.hash = 0xcbf29ce484222325ull;
-  R.infeasible = R.routed = R.sum_q = R.sum_w = 0;
-  R.status = RS_REPLAY_FINISHED;
-  R.err_inst = -1;
-  R.rng_pos = 312;
-  R.a_base = 0;
-  R.h_base = -2 * kWarp;
-  R.h_prompt = R.h_true = R.h_bucket = 0;
-  if (POL == RS_POLICY_RL && P.rl_eps > 0.0)
-    mt_seed_warp(G.rng, P.policy_seed ? P.policy_seed[r] : 0ull);
-  __syncwarp();
-  load_arrival_window(P, R);
-  if (bad) {
-    R.status = RS_REPLAY_INVALID_TRACE;
-  } else {
-    inject(P, R);  // ctor (env.hpp:193)
-  }
-
-  // ---------------------------------------------------------- tick loop
-  while (R.status == RS_REPLAY_FINISHED && R.completed != R.n && R.tick < P.max_ticks) {
-    if (POL == RS_POLICY_MIN_MIN && queue_len<POL>(R) > 0) {
-      if (!minmin_pick(P, G, R)) { R.status = RS_REPLAY_CAPACITY; break; }
-    }
-    const bool has_head = queue_len<POL>(R) > 0;
-    Rec hr;
-    int hb = 0;
-    if (has_head) {
-      hr = head_rec<POL>(P, G, R, &hb);
-    } else {
-      hr.req = hr.prompt = hr.dhat = hr.tru = hr.emit = 0;
-    }
-    const int action = decide<POL>(P, G, M, R, has_head, hr, hb);
-    R.hash = hash_action(R.hash, action);
-    if (action < 0 || action > m) { R.status = RS_REPLAY_BAD_ACTION; break; }
-    const double t1 = __dadd_rn(R.clock, P.delta_t);
-    if (action < m && has_head) {
-      if ((long long)hr.prompt + hr.tru > P.kv_cap) {
-        R.infeasible++;  // env.hpp:262-267: flagged, stays queued
-      } else {
-        if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) {
-          if (l == 0)
-            for (int k = 0; k + 1 < R.nfront; ++k) G.front[k] = G.front[k + 1];
-          __syncwarp();
-          R.nfront--;
-        } else {
-          R.qhead++;
-          if (POL == RS_POLICY_MIN_MIN) mm_skip_removed(P, R);
-        }
-        if (l == 0) {
-          P.o_routed[R.off + hr.req] = R.clock;
-          P.o_instance[R.off + hr.req] = action;
-        }
-        R.routed++;
-        InstHot h = load_inst(G, action);  // Instance::enqueue
-        if (h.clock < R.clock) h.clock = R.clock;
-        wait_push_back(P, G, R.off, action, h, hr);
-        store_inst(G, action, h);
-        R.total_wait++;
-      }
-    }
-    // run_until(t1) for every instance, index order (independent)
-    int comps = 0;
-    for (int g = 0; g < m && R.status == RS_REPLAY_FINISHED; g += kWarp) {
-      const int i = g + l;
-      bool busy = false;
-      if (i < m) {
-        const InstHot& hi = G.inst[i];
-        if (hi.clock < t1) {
-          if (hi.n_run > 0 || hi.w_cnt > 0) busy = true;
-          else G.inst[i].clock = t1;  // idle instance skips ahead
-        }
-      }
-      unsigned mask = __ballot_sync(kFull, busy);
-      __syncwarp();
-      while (mask) {
-        const int ii = g + __ffs(mask) - 1;
-        mask &= mask - 1;
-        InstHot h = load_inst(G, ii);
-        const int w0 = h.w_cnt + h.o_cnt;
-        while (h.clock < t1 && (h.n_run > 0 || h.w_cnt > 0)) {
-          const int c = inst_step<NEED_DBC>(P, G, R.off, ii, h);
-          if (c < 0) {
-            R.status = RS_REPLAY_NOT_ADMISSIBLE;
-            R.err_inst = ii;
-            break;
-          }
-          comps += c;
-        }
-        if (h.n_run == 0 && h.w_cnt == 0 && h.clock < t1) h.clock = t1;
-        R.total_wait += h.w_cnt + h.o_cnt - w0;
-        store_inst(G, ii, h);
-        if (R.status != RS_REPLAY_FINISHED) break;
-      }
-    }
-    if (R.status != RS_REPLAY_FINISHED) break;
-    R.completed += comps;
-    R.clock = t1;
-    inject(P, R);
-    R.tick++;
-    R.sum_q += queue_len<POL>(R);
-    R.sum_w += R.total_wait;
-  }
-  if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
-
-  // ------------------------------------------------- statistics (metrics.hpp)
   double se = 0.0, st = 0.0, sb = 0.0, sw = 0.0;
   long long tbtc = 0, pre = 0, tok = 0;
   double fa = __longlong_as_double(0x7fefffffffffffffll), lc = 0.0;
@@ -578,6 +431,159 @@ __device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int
     P.stats[r] = s;
   }
   __syncwarp();
+}
+
+template <int POL>
+__device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int r) {
+  constexpr bool NEED_DBC = POL == RS_POLICY_RL;
+  const int l = lane_id();
+  Replay R;
+  R.off = P.offsets[r];
+  R.n = (int)(P.offsets[r + 1] - R.off);
+  const int m = P.m;
+
+  // outputs to the reference's "not yet" values; input checks
+  bool bad = false;
+  for (int j = l; j < R.n; j += kWarp) {
+    const long long g = R.off + j;
+    P.o_instance[g] = -1;
+    P.o_routed[g] = -1.0;
+    P.o_first[g] = -1.0;
+    P.o_completion[g] = -1.0;
+    P.o_preempt[g] = 0;
+    if (POL == RS_POLICY_MIN_MIN) P.mm_removed[g] = 0;
+    const int p = P.prompt[g], d = P.decode[g];
+    if (p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens) bad = true;
+    if (j > 0 && P.arrival[g] < P.arrival[g - 1]) bad = true;
+  }
+  bad = __any_sync(kFull, bad);
+  for (int i = l; i < m; i += kWarp) {
+    InstHot h;
+    h.clock = 0.0;
+    h.res_wait = h.pend_wait = h.dleft_wait = h.tleft_wait = h.tok_wait = 0;
+    h.n_run = h.n_prefill = h.res_run = h.kv_run = h.pend_run = 0;
+    h.dleft_run = h.tleft_run = h.tok_run = 0;
+    h.min_dleft = 0x7fffffff;
+    h.w_head = h.w_cnt = h.o_cnt = 0;
+    h.o_head = h.o_tail = (int)kNil;
+    h._pad0 = h._pad1 = 0;
+    G.inst[i] = h;
+    if (NEED_DBC)
+      for (int b = 0; b < RS_MAX_BUCKETS; ++b) G.dbc[i * RS_MAX_BUCKETS + b] = 0;
+  }
+  R.clock = 0.0;
+  R.tick = 0;
+  R.qhead = R.cursor = 0;
+  R.completed = 0;
+  R.nfront = R.n_removed = 0;
+  R.total_wait = 0;
+  R.rr_next = R.dsl_next = 0;
+  R.mc_next = 0.0;
+  R.hash = 0xcbf29ce484222325ull;
+  R.infeasible = R.routed = R.sum_q = R.sum_w = 0;
+  R.status = RS_REPLAY_FINISHED;
+  R.err_inst = -1;
+  R.rng_pos = 312;
+  R.a_base = 0;
+  R.h_base = -2 * kWarp;
+  R.h_prompt = R.h_true = R.h_bucket = 0;
+  if (POL == RS_POLICY_RL && P.rl_eps > 0.0)
+    mt_seed_warp(G.rng, P.policy_seed ? P.policy_seed[r] : 0ull);
+  __syncwarp();
+  load_arrival_window(P, R);
+  if (bad) {
+    R.status = RS_REPLAY_INVALID_TRACE;
+  } else {
+    inject(P, R);  // ctor (env.hpp:193)
+  }
+
+  // ---------------------------------------------------------- tick loop
+  while (R.status == RS_REPLAY_FINISHED && R.completed != R.n && R.tick < P.max_ticks) {
+    if (POL == RS_POLICY_MIN_MIN && queue_len<POL>(R) > 0) {
+      if (!minmin_pick(P, G.front, R)) { R.status = RS_REPLAY_CAPACITY; break; }
+    }
+    const bool has_head = queue_len<POL>(R) > 0;
+    Rec hr;
+    int hb = 0;
+    if (has_head) {
+      hr = head_rec<POL>(P, G.front, R, &hb);
+    } else {
+      hr.req = hr.prompt = hr.dhat = hr.tru = hr.emit = 0;
+    }
+    const int action = decide<POL>(P, G, M, R, has_head, hr, hb);
+    R.hash = hash_action(R.hash, action);
+    if (action < 0 || action > m) { R.status = RS_REPLAY_BAD_ACTION; break; }
+    const double t1 = __dadd_rn(R.clock, P.delta_t);
+    if (action < m && has_head) {
+      if ((long long)hr.prompt + hr.tru > P.kv_cap) {
+        R.infeasible++;  // env.hpp:262-267: flagged, stays queued
+      } else {
+        if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) {
+          if (l == 0)
+            for (int k = 0; k + 1 < R.nfront; ++k) G.front[k] = G.front[k + 1];
+          __syncwarp();
+          R.nfront--;
+        } else {
+          R.qhead++;
+          if (POL == RS_POLICY_MIN_MIN) mm_skip_removed(P, R);
+        }
+        if (l == 0) {
+          P.o_routed[R.off + hr.req] = R.clock;
+          P.o_instance[R.off + hr.req] = action;
+        }
+        R.routed++;
+        InstHot h = load_inst(G, action);  // Instance::enqueue
+        if (h.clock < R.clock) h.clock = R.clock;
+        wait_push_back(P, G, R.off, action, h, hr);
+        store_inst(G, action, h);
+        R.total_wait++;
+      }
+    }
+    // run_until(t1) for every instance, index order (independent)
+    int comps = 0;
+    for (int g = 0; g < m && R.status == RS_REPLAY_FINISHED; g += kWarp) {
+      const int i = g + l;
+      bool busy = false;
+      if (i < m) {
+        const InstHot& hi = G.inst[i];
+        if (hi.clock < t1) {
+          if (hi.n_run > 0 || hi.w_cnt > 0) busy = true;
+          else G.inst[i].clock = t1;  // idle instance skips ahead
+        }
+      }
+      unsigned mask = __ballot_sync(kFull, busy);
+      __syncwarp();
+      while (mask) {
+        const int ii = g + __ffs(mask) - 1;
+        mask &= mask - 1;
+        InstHot h = load_inst(G, ii);
+        const int w0 = h.w_cnt + h.o_cnt;
+        while (h.clock < t1 && (h.n_run > 0 || h.w_cnt > 0)) {
+          const int c = inst_step<NEED_DBC>(P, G, R.off, ii, h);
+          if (c < 0) {
+            R.status = RS_REPLAY_NOT_ADMISSIBLE;
+            R.err_inst = ii;
+            break;
+          }
+          comps += c;
+        }
+        if (h.n_run == 0 && h.w_cnt == 0 && h.clock < t1) h.clock = t1;
+        R.total_wait += h.w_cnt + h.o_cnt - w0;
+        store_inst(G, ii, h);
+        if (R.status != RS_REPLAY_FINISHED) break;
+      }
+    }
+    if (R.status != RS_REPLAY_FINISHED) break;
+    R.completed += comps;
+    R.clock = t1;
+    inject(P, R);
+    R.tick++;
+    R.sum_q += queue_len<POL>(R);
+    R.sum_w += R.total_wait;
+  }
+  if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
+
+  write_replay_stats(P, R, r);
 }
 
 template <int POL>

@@ -226,4 +226,19 @@ rs_status rs_generate_mixture_batch(const rs_profile* profile, const rs_threshol
   return RS_OK;
 }
 
+rs_status rs_mlp_random_init(const int32_t* dims, int32_t num_layers, uint64_t seed,
+                             double* params_out) {
+  if (!dims || !params_out || num_layers < 1) return RS_ERR_INVALID_ARGUMENT;
+  Source s(seed);
+  double* p = params_out;
+  for (int l = 0; l < num_layers; ++l) {
+    const double scale = std::sqrt(2.0 / static_cast<double>(dims[l]));
+    const size_t wn = static_cast<size_t>(dims[l]) * static_cast<size_t>(dims[l + 1]);
+    for (size_t i = 0; i < wn; ++i) p[i] = (2.0 * s.uniform() - 1.0) * scale;
+    for (int o = 0; o < dims[l + 1]; ++o) p[wn + o] = 0.0;
+    p += wn + dims[l + 1];
+  }
+  return RS_OK;
+}
+
 }  // extern "C"

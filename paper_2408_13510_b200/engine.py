@@ -215,3 +215,13 @@ def mlp_forward(dims, params, states: np.ndarray, device: int = 0):
                                            g.ctypes.data, device))
     del keep
     return q, g
+
+
+def mlp_random_init(dims, seed: int) -> np.ndarray:
+    """DqnAgent(state_dim, actions, {hidden}, seed)'s online network weights
+    (Mlp::random, mlp.hpp:32-45), reference flat layout."""
+    lib = abi.load_library()
+    d = np.ascontiguousarray(dims, dtype=np.int32)
+    p = np.empty(abi.mlp_param_count(list(dims)), np.float64)
+    abi.check(lib, lib.rs_mlp_random_init(d.ctypes.data, len(dims) - 1, int(seed), p.ctypes.data))
+    return p

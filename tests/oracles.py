@@ -71,7 +71,7 @@ def ref_lib() -> C.CDLL:
         lib.ref_run_replay.argtypes = [P(abi.BatchCfg), C.c_int64] + [C.c_void_p] * 4 + [
             C.c_uint64, C.c_uint64] + [C.c_void_p] * 8 + [C.c_int64]
         lib.ref_run_batch.restype = C.c_double
-        lib.ref_run_batch.argtypes = [P(abi.BatchCfg), C.c_int32] + [C.c_void_p] * 8 + [
+        lib.ref_run_batch.argtypes = [P(abi.BatchCfg), C.c_int32] + [C.c_void_p] * 7 + [
             C.c_int32, C.c_void_p]
         lib.ref_agent_init.restype = C.c_int64
         lib.ref_agent_init.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p,

@@ -18,6 +18,17 @@ pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
+@pytest.fixture(params=["fast", "general"], autouse=True)
+def kernel_path(request, monkeypatch):
+    """Every parity test runs on both replay kernels: the lane-per-instance
+    fast kernel (whole-prompt prefill) and the general warp-per-instance one."""
+    if request.param == "general":
+        monkeypatch.setenv("RS_FORCE_GENERAL", "1")
+    else:
+        monkeypatch.delenv("RS_FORCE_GENERAL", raising=False)
+    return request.param
+
+
 def run_engine(lib, cfg, traces, pseeds, qseeds=None):
     tb = engine.TraceBatch.from_traces(traces)
     N, R = tb.total, tb.num_replays
@@ -179,7 +190,7 @@ def test_golden_summary_on_gpu(gpu):
 
 def test_mlp_forward_kernel_matches_oracle(gpu):
     rng = np.random.default_rng(9)
-    for dims in ([27, 64, 64, 5], [51, 64, 64, 9], [387, 128, 128, 65], [9, 3, 2]):
+    for dims in ([27, 64, 64, 5], [51, 64, 64, 9], [387, 128, 128, 65], [9, 3, 2]):  # m=64: 387 wide
         p = rng.standard_normal(abi.mlp_param_count(dims))
         x = rng.standard_normal((257, dims[0]))
         x[rng.random(x.shape) < 0.5] = 0.0
