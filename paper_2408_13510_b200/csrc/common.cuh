@@ -82,6 +82,7 @@ struct KParams {
   const double* rl_w;               // reference flat layout (device)
   int rl_maxw;                     // widest hidden layer
   int smem_weights_bytes;          // staged W^T + b at the start of smem
+  const double* rl_wt_global;      // W^T + b in global memory (nets too big for smem)
   // trace (CSR over replays)
   int num_replays;
   const long long* offsets;
@@ -108,11 +109,33 @@ struct KParams {
   // shared-memory layout (bytes, per replay group)
   int smem_group_bytes;
   int off_run, off_wait, off_dbc, off_rlx, off_rng, off_front;
+  // fast kernel: word offsets (relative to the group base) of the running
+  // entry fields and waiting-ring fields, per-instance running stride, and
+  // the power-of-two lane width covering the instances (argmin reductions)
+  int f_rreq, f_rprompt, f_rdhat, f_rtrue, f_rkey;
+  int f_wreq, f_wprompt, f_wdhat, f_wtrue, f_wemit;
+  int rstride, mwidth;
+  // Divisors that are exact powers of two divide by an exact reciprocal
+  // multiply (IEEE scaling: bit-identical to the division).
+  double inv_eps, inv_kv, inv_mb;
+  int eps_pow2, kv_pow2, mb_pow2;
+  int ub_max;  // largest upper_bound_tokens (32-bit aggregate guard)
 };
+
+// x / c, correctly rounded; a multiply when c is a power of two.
+__device__ __forceinline__ double div_exact(double x, double c, double inv_c, int pow2) {
+  return pow2 ? __dmul_rn(x, inv_c) : __ddiv_rn(x, c);
+}
 
 // ---------------------------------------------------------------- helpers
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & (kWarp - 1); }
+// Lane id the compiler cannot rematerialize (no repeated S2R SR_TID.X).
+__device__ __forceinline__ int opaque_lane() {
+  int l = threadIdx.x & (kWarp - 1);
+  asm volatile("" : "+r"(l));
+  return l;
+}
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -148,8 +171,7 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
 }
 
 // Inclusive prefix sum across the warp.
-__device__ __forceinline__ int warp_incl_scan(int v) {
-  const int l = lane_id();
+__device__ __forceinline__ int warp_incl_scan(int v, int l) {
 #pragma unroll
   for (int o = 1; o < kWarp; o <<= 1) {
     int t = __shfl_up_sync(kFull, v, o);
@@ -198,8 +220,7 @@ __device__ __forceinline__ unsigned long long hash_action(unsigned long long h, 
 // `s` holds the 312-word state.  Three dependency phases of the twist
 // (i < 156 reads only old words; 156 <= i < 311 reads new s[i-156]; i = 311
 // reads new s[0]), then tempering.
-__device__ inline void mt_twist_warp(unsigned long long* s) {
-  const int l = lane_id();
+__device__ inline void mt_twist_warp(unsigned long long* s, int l) {
   auto tw = [](unsigned long long a, unsigned long long b) {
     unsigned long long x = (a & 0xFFFFFFFF80000000ull) | (b & 0x7FFFFFFFull);
     unsigned long long xa = x >> 1;
@@ -244,8 +265,8 @@ __device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
 }
 
 // Seeding (std::mt19937_64 constructor); serial recurrence, lane 0.
-__device__ inline void mt_seed_warp(unsigned long long* s, unsigned long long seed) {
-  if (lane_id() == 0) {
+__device__ inline void mt_seed_warp(unsigned long long* s, unsigned long long seed, int l) {
+  if (l == 0) {
     s[0] = seed;
     for (int i = 1; i < 312; ++i)
       s[i] = 6364136223846793005ull * (s[i - 1] ^ (s[i - 1] >> 62)) + (unsigned long long)i;

@@ -203,11 +203,22 @@ int64_t heavy_cutoff(const rs_profile& p, const rs_thresholds& t) {
 }
 
 struct WsLayout {
-  size_t counter, next, prev, emit, removed, total;
+  size_t counter, next, prev, emit, removed, wt, total;
 };
-WsLayout ws_layout(int64_t total_requests) {
+
+size_t rl_param_count(const rs_batch_cfg& c) {
+  if (c.policy != RS_POLICY_RL) return 0;
+  size_t w = 0;
+  for (int l = 0; l < c.rl_num_layers; ++l)
+    w += (size_t)c.rl_dims[l] * c.rl_dims[l + 1] + c.rl_dims[l + 1];
+  return w;
+}
+
+WsLayout ws_layout(int64_t total_requests, size_t rl_params = 0) {
   WsLayout w;
   size_t off = 0;
+  w.wt = off;  // transposed Q-network (global-weights mode), may be empty
+  off = align_up(off + rl_params * sizeof(double), 256);
   w.counter = off;
   off = align_up(off + 256, 256);
   w.next = off;
@@ -357,7 +368,7 @@ rs_status rs_workspace_size(const rs_batch_cfg* cfg, int32_t num_replays,
   if (s != RS_OK) return s;
   if (!bytes || num_replays < 0 || total_requests < 0)
     return fail(RS_ERR_INVALID_ARGUMENT, "bad workspace query");
-  *bytes = ws_layout(total_requests).total;
+  *bytes = ws_layout(total_requests, rl_param_count(*cfg)).total;
   return RS_OK;
 }
 
@@ -427,16 +438,22 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
     return fail(RS_ERR_INVALID_ARGUMENT, "rs_replay_batch needs every per-request output array");
   if (cfg->policy == RS_POLICY_RL && cfg->rl_epsilon > 0.0 && !tr->policy_seed)
     return fail(RS_ERR_INVALID_ARGUMENT, "epsilon-greedy needs trace->policy_seed");
-  const WsLayout wl = ws_layout(tr->total_requests);
+  const WsLayout wl = ws_layout(tr->total_requests, rl_param_count(*cfg));
   if (!workspace || workspace_bytes < wl.total)
     return fail(RS_ERR_INVALID_ARGUMENT, "workspace too small (rs_workspace_size)");
   cudaStream_t st = (cudaStream_t)stream;
   char* ws = static_cast<char*>(workspace);
 
-  const int wcap = std::max(8, std::min(128, env_int("RS_WAIT_RING", 64)));
-  // whole-prompt prefill (no chunking) takes the lane-per-instance kernel
-  const bool fast = cfg->chunk_size == 0 && env_int("RS_FORCE_GENERAL", 0) == 0;
-  const int groups = cfg->num_instances <= 32 ? 1 : (cfg->num_instances <= 64 ? 2 : 4);
+  // shared waiting-ring slots per instance (the rest of a long queue lives
+  // in the global overflow list): smaller rings for larger fleets keep
+  // several replays resident per SM
+  const int m_inst = cfg->num_instances;
+  const int wdef = m_inst <= 16 ? 64 : (m_inst <= 32 ? 32 : 16);
+  const int wcap = std::max(8, std::min(128, env_int("RS_WAIT_RING", wdef)));
+  // whole-prompt prefill (no chunking, m <= 64) takes the lane-per-instance
+  // kernel; chunked prefill and larger fleets take the general kernel
+  const bool fast = cfg->chunk_size == 0 && m_inst <= 64 && env_int("RS_FORCE_GENERAL", 0) == 0;
+  const int groups = m_inst <= 32 ? 1 : 2;
   Layout L = make_layout(*cfg, wcap, fast);
   rs::KParams kp;
   std::memset(&kp, 0, sizeof(kp));
@@ -508,6 +525,35 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
   kp.off_rlx = L.off_rlx;
   kp.off_rng = L.off_rng;
   kp.off_front = L.off_front;
+  {  // fast-kernel word offsets (fast.cuh RQ/RP/.../WE accessors)
+    const int m = cfg->num_instances;
+    kp.rstride = L.rcap | 1;
+    kp.f_rreq = L.off_run / 4;
+    kp.f_rprompt = kp.f_rreq + m * kp.rstride;
+    kp.f_rdhat = kp.f_rprompt + m * kp.rstride;
+    kp.f_rtrue = kp.f_rdhat + m * kp.rstride;
+    kp.f_rkey = kp.f_rtrue + m * kp.rstride;
+    kp.f_wreq = L.off_wait / 4;
+    kp.f_wprompt = kp.f_wreq + m * L.wcap;
+    kp.f_wdhat = kp.f_wprompt + m * L.wcap;
+    kp.f_wtrue = kp.f_wdhat + m * L.wcap;
+    kp.f_wemit = kp.f_wtrue + m * L.wcap;
+    kp.mwidth = 1;
+    while (kp.mwidth < m && kp.mwidth < rs::kWarp) kp.mwidth <<= 1;
+  }
+  {  // power-of-two divisors -> exact reciprocal multiplies
+    auto pow2 = [](double c, double* inv) {
+      int e = 0;
+      const double f = std::frexp(c, &e);
+      *inv = 1.0 / c;
+      return (f == 0.5 && e > -1000 && e < 1000) ? 1 : 0;
+    };
+    kp.eps_pow2 = pow2(cfg->impact.epsilon_s, &kp.inv_eps);
+    kp.kv_pow2 = pow2((double)cfg->kv_capacity_tokens, &kp.inv_kv);
+    kp.mb_pow2 = pow2((double)cfg->max_batch_size, &kp.inv_mb);
+    kp.ub_max = 0;
+    for (int b = 0; b < cfg->n_predictor_edges; ++b) kp.ub_max = std::max(kp.ub_max, kp.ub[b]);
+  }
 
   // warps (replays) per block: maximise resident warps per SM; the RL
   // weights are staged once per block, which favours wider blocks.
@@ -516,6 +562,34 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
   int smem_optin = 0;
   RS_CUDA(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
   const int smem_sm = 228 * 1024;
+  // Q-networks that leave fewer than 4 replay slots per SM next to their
+  // staged weights, or with a layer wider than the shared-memory forward's
+  // masks, run from a transposed copy in global memory (L2-resident).
+  int max_dim = 0;
+  for (int l = 0; l <= cfg->rl_num_layers && cfg->policy == RS_POLICY_RL; ++l)
+    max_dim = std::max(max_dim, cfg->rl_dims[l]);
+  const bool rl_global = cfg->policy == RS_POLICY_RL &&
+                         (env_int("RS_RL_GLOBAL", 0) != 0 || max_dim > rs::kMlpSmemMaxWidth ||
+                          L.weights_bytes + 4 * L.group_bytes > smem_optin);
+  if (rl_global) {
+    double* wt = reinterpret_cast<double*>(ws + wl.wt);
+    const size_t np = rl_param_count(*cfg);
+    rs::MlpTransposeArgs ta;
+    ta.params = cfg->rl_params;
+    ta.layers = cfg->rl_num_layers;
+    for (int l = 0; l <= RS_MAX_LAYERS; ++l) ta.dims[l] = cfg->rl_dims[l];
+    for (int l = 0; l < RS_MAX_LAYERS; ++l) {
+      ta.woff[l] = L.woff[l];
+      ta.boff[l] = L.boff[l];
+    }
+    ta.out = wt;
+    ta.count = np;
+    rs::mlp_transpose_kernel<0><<<(unsigned)((np + 255) / 256), 256, 0, st>>>(ta);
+    RS_CUDA(cudaGetLastError());
+    kp.rl_wt_global = wt;
+    kp.smem_weights_bytes = 0;
+    L.weights_bytes = 0;
+  }
   int best_wpb = 0, best_warps = 0;
   const int wpb_env = env_int("RS_WARPS_PER_BLOCK", 0);
   for (int wpb = 8; wpb >= 1; --wpb) {

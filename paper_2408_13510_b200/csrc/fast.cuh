@@ -12,69 +12,80 @@
 // clock += dtb + dpt*n, D += 1, and the aggregates move by closed forms
 // (kv += n, true-left -= n, token mass += n, reservations += #overrun,
 // decode-left -= n - #overrun).  Per-entry work happens only at EVENTS:
-//   * the first decode step after admission  -> first-token stores,
-//   * D == min(true - key)                    -> completions (scan),
-//   * D == min(dhat - key) (emitted reaches the estimate) -> re-count,
-//   * KV overflow                             -> preemption.
+//   * the first decode step after admission  -> first-token stores (lane),
+//   * D == min(true - key)                    -> completions (warp scan),
+//   * D == min(dhat - key) (emitted reaches the estimate) -> warp re-count,
+//   * KV overflow                             -> preemption (lane).
 // Each lane owns one instance (<= 32 per group, G groups per lane), so all
-// instances of a replay advance in parallel; events are handled by the whole
-// warp.  A replay that raises "nothing admissible" is re-run with
-// instances stepped one at a time in index order, reproducing exactly where
-// the reference's exception stops a tick.
+// instances of a replay advance in parallel.  A replay that raises "nothing
+// admissible" is re-run with instances stepped one at a time in index order,
+// reproducing exactly where the reference's exception stops a tick.
+//
+// Shared memory is addressed as one int array from a single per-warp word
+// base (`gw`, laundered so the compiler keeps it in a register) plus the
+// per-field word offsets of KParams (constant bank), and the lane id is
+// likewise computed once: no pointer structs to rematerialize with S2R.
 #pragma once
 
 #include "router.cuh"
 
 namespace rs {
 
-constexpr int kFresh = 0x40000000;       // entry awaits its first token
+extern __shared__ __align__(16) int rs_smw[];
+
+constexpr int kFresh = 0x40000000;  // entry awaits its first token
 constexpr int kReqMask = 0x3fffffff;
 constexpr int kBig = 0x7fffffff;
 
 struct Inst {  // one instance, held in its lane's registers
   double clock;
+  double dec_el;  // decode_batch_time for el_n running (cached)
+  int el_n;
   int D, n, npf, ft;
   int res, kv, pend, dleft, tleft, tok, nge, next_ge, next_done;
   int w_head, w_cnt, o_cnt, o_head, o_tail;
   int comps;
-  long long resw, pendw, dlw, tlw, tokw;
+  // waiting-queue aggregates in 32 bits: run_replay_fast refuses replays
+  // whose N x max(prompt + max(decode, bucket bound)) could reach 2^31
+  int resw, pendw, dlw, tlw, tokw;
 };
 
-struct FRun {  // running entries, admission order, stride per instance
-  int *req, *prompt, *dhat, *tru, *key;
-  int stride;
-};
-
-struct FastGrp {
-  FRun R;
-  int *w_req, *w_prompt, *w_dhat, *w_true, *w_emit;
-  int wstride;
-  double* rlx;
-  unsigned long long* rng;
-  int* front;
-};
-
-__device__ __forceinline__ FastGrp make_fast_grp(const KParams& P, char* base) {
-  FastGrp G;
-  const int rs_ = P.rcap | 1, ws_ = P.wcap;
-  int* run = reinterpret_cast<int*>(base + P.off_run);
-  const int mr = P.m * rs_;
-  G.R.req = run; G.R.prompt = run + mr; G.R.dhat = run + 2 * mr; G.R.tru = run + 3 * mr;
-  G.R.key = run + 4 * mr;
-  G.R.stride = rs_;
-  int* wt = reinterpret_cast<int*>(base + P.off_wait);
-  const int mw = P.m * ws_;
-  G.w_req = wt; G.w_prompt = wt + mw; G.w_dhat = wt + 2 * mw; G.w_true = wt + 3 * mw;
-  G.w_emit = wt + 4 * mw;
-  G.wstride = ws_;
-  G.rlx = reinterpret_cast<double*>(base + P.off_rlx);
-  G.rng = reinterpret_cast<unsigned long long*>(base + P.off_rng);
-  G.front = reinterpret_cast<int*>(base + P.off_front);
-  return G;
+// running entry fields (admission order) and waiting ring fields
+__device__ __forceinline__ int& RQ(const KParams& P, int gw, int i, int j) {
+  return rs_smw[gw + P.f_rreq + i * P.rstride + j];
+}
+__device__ __forceinline__ int& RP(const KParams& P, int gw, int i, int j) {
+  return rs_smw[gw + P.f_rprompt + i * P.rstride + j];
+}
+__device__ __forceinline__ int& RD(const KParams& P, int gw, int i, int j) {
+  return rs_smw[gw + P.f_rdhat + i * P.rstride + j];
+}
+__device__ __forceinline__ int& RT(const KParams& P, int gw, int i, int j) {
+  return rs_smw[gw + P.f_rtrue + i * P.rstride + j];
+}
+__device__ __forceinline__ int& RK(const KParams& P, int gw, int i, int j) {
+  return rs_smw[gw + P.f_rkey + i * P.rstride + j];
+}
+__device__ __forceinline__ int& WQ(const KParams& P, int gw, int i, int s) {
+  return rs_smw[gw + P.f_wreq + i * P.wcap + s];
+}
+__device__ __forceinline__ int& WP(const KParams& P, int gw, int i, int s) {
+  return rs_smw[gw + P.f_wprompt + i * P.wcap + s];
+}
+__device__ __forceinline__ int& WD(const KParams& P, int gw, int i, int s) {
+  return rs_smw[gw + P.f_wdhat + i * P.wcap + s];
+}
+__device__ __forceinline__ int& WT(const KParams& P, int gw, int i, int s) {
+  return rs_smw[gw + P.f_wtrue + i * P.wcap + s];
+}
+__device__ __forceinline__ int& WE(const KParams& P, int gw, int i, int s) {
+  return rs_smw[gw + P.f_wemit + i * P.wcap + s];
 }
 
 __device__ __forceinline__ void inst_init(Inst& I) {
   I.clock = 0.0;
+  I.dec_el = 0.0;
+  I.el_n = -1;
   I.D = I.n = I.npf = I.ft = 0;
   I.res = I.kv = I.pend = I.dleft = I.tleft = I.tok = I.nge = 0;
   I.next_ge = I.next_done = kBig;
@@ -125,37 +136,35 @@ __device__ __forceinline__ void lane_ov_unlink(const KParams& P, long long off, 
   I.o_cnt--;
 }
 
-__device__ __forceinline__ void lane_ring_put(const FastGrp& G, int i, int slot, int req, int prompt,
-                                              int dhat, int tru, int emit) {
-  const int b = i * G.wstride + slot;
-  G.w_req[b] = req;
-  G.w_prompt[b] = prompt;
-  G.w_dhat[b] = dhat;
-  G.w_true[b] = tru;
-  G.w_emit[b] = emit;
+__device__ __forceinline__ void ring_put(const KParams& P, int gw, int i, int s, int req, int prompt,
+                                         int dhat, int tru, int emit) {
+  WQ(P, gw, i, s) = req;
+  WP(P, gw, i, s) = prompt;
+  WD(P, gw, i, s) = dhat;
+  WT(P, gw, i, s) = tru;
+  WE(P, gw, i, s) = emit;
 }
 
-__device__ __forceinline__ void lane_refill(const KParams& P, const FastGrp& G, long long off, int i,
-                                            Inst& I) {
+__device__ __forceinline__ void lane_refill(const KParams& P, int gw, long long off, int i, Inst& I) {
   if (I.o_cnt == 0 || I.w_cnt >= P.wcap) return;
   const int req = I.o_head;
   const int prompt = P.prompt[off + req], tru = P.decode[off + req];
   const int dhat = P.ub[P.bucket[off + req]], emit = P.ov_emit[off + req];
   lane_ov_unlink(P, off, I, req);
-  int slot = I.w_head + I.w_cnt;
-  if (slot >= P.wcap) slot -= P.wcap;
-  lane_ring_put(G, i, slot, req, prompt, dhat, tru, emit);
+  int s = I.w_head + I.w_cnt;
+  if (s >= P.wcap) s -= P.wcap;
+  ring_put(P, gw, i, s, req, prompt, dhat, tru, emit);
   I.w_cnt++;
 }
 
 // Instance::enqueue (instance.hpp:113-130) by the owning lane.
-__device__ __forceinline__ void lane_enqueue(const KParams& P, const FastGrp& G, long long off,
-                                             int i, Inst& I, const Rec& r, double now) {
+__device__ __forceinline__ void lane_enqueue(const KParams& P, int gw, long long off, int i, Inst& I,
+                                             const Rec& r, double now) {
   if (I.clock < now) I.clock = now;
   if (I.o_cnt == 0 && I.w_cnt < P.wcap) {
-    int slot = I.w_head + I.w_cnt;
-    if (slot >= P.wcap) slot -= P.wcap;
-    lane_ring_put(G, i, slot, r.req, r.prompt, r.dhat, r.tru, 0);
+    int s = I.w_head + I.w_cnt;
+    if (s >= P.wcap) s -= P.wcap;
+    ring_put(P, gw, i, s, r.req, r.prompt, r.dhat, r.tru, 0);
     I.w_cnt++;
   } else {
     lane_ov_push_back(P, off, I, r.req, 0);
@@ -163,31 +172,30 @@ __device__ __forceinline__ void lane_enqueue(const KParams& P, const FastGrp& G,
   waitagg(I, r.prompt, r.dhat, r.tru, 0, +1);
 }
 
-__device__ __forceinline__ void lane_push_front(const KParams& P, const FastGrp& G, long long off,
-                                                int i, Inst& I, int req, int prompt, int dhat,
-                                                int tru, int emit) {
+__device__ __forceinline__ void lane_push_front(const KParams& P, int gw, long long off, int i,
+                                                Inst& I, int req, int prompt, int dhat, int tru,
+                                                int emit) {
   if (I.w_cnt == P.wcap) {  // spill the ring's back element to the overflow front
     int s = I.w_head + I.w_cnt - 1;
     if (s >= P.wcap) s -= P.wcap;
-    const int b = i * G.wstride + s;
-    lane_ov_push_front(P, off, I, G.w_req[b], G.w_emit[b]);
+    lane_ov_push_front(P, off, I, WQ(P, gw, i, s), WE(P, gw, i, s));
     I.w_cnt--;
   }
   I.w_head = I.w_head == 0 ? P.wcap - 1 : I.w_head - 1;
-  lane_ring_put(G, i, I.w_head, req, prompt, dhat, tru, emit);
+  ring_put(P, gw, i, I.w_head, req, prompt, dhat, tru, emit);
   I.w_cnt++;
   waitagg(I, prompt, dhat, tru, emit, +1);
 }
 
 // Append an admitted request to the running batch (instance.hpp:187-192).
-__device__ __forceinline__ void lane_admit_one(const FastGrp& G, int i, Inst& I, int req,
+__device__ __forceinline__ void lane_admit_one(const KParams& P, int gw, int i, Inst& I, int req,
                                                int prompt, int dhat, int tru, int emit) {
-  const int b = i * G.R.stride + I.n;
-  G.R.req[b] = req | (emit == 0 ? kFresh : 0);
-  G.R.prompt[b] = prompt;
-  G.R.dhat[b] = dhat;
-  G.R.tru[b] = tru;
-  G.R.key[b] = emit - I.D;
+  const int j = I.n;
+  RQ(P, gw, i, j) = req | (emit == 0 ? kFresh : 0);
+  RP(P, gw, i, j) = prompt;
+  RD(P, gw, i, j) = dhat;
+  RT(P, gw, i, j) = tru;
+  RK(P, gw, i, j) = emit - I.D;
   I.n++;
   I.npf++;
   I.res += reserved_of(prompt, dhat, emit);
@@ -205,33 +213,32 @@ __device__ __forceinline__ void lane_admit_one(const FastGrp& G, int i, Inst& I,
 }
 
 // Instance::admit_waiting (instance.hpp:149-195) by the owning lane.
-__device__ inline void lane_admit(const KParams& P, const FastGrp& G, long long off, int i,
-                                  Inst& I) {
+__device__ inline void lane_admit(const KParams& P, int gw, long long off, int i, Inst& I) {
   while (I.w_cnt > 0 && I.n < P.max_batch) {
-    if (P.batching == RS_BATCHING_FCFS) {
-      const int b = i * G.wstride + I.w_head;
-      const int prompt = G.w_prompt[b], dhat = G.w_dhat[b], emit = G.w_emit[b];
+    if (P.batching == RS_BATCHING_FCFS) {  // strict head of line
+      const int s = I.w_head;
+      const int prompt = WP(P, gw, i, s), dhat = WD(P, gw, i, s), emit = WE(P, gw, i, s);
       if (I.res + reserved_of(prompt, dhat, emit) > P.kv_cap) break;
-      const int req = G.w_req[b], tru = G.w_true[b];
-      I.w_head = I.w_head + 1 == P.wcap ? 0 : I.w_head + 1;
+      const int req = WQ(P, gw, i, s), tru = WT(P, gw, i, s);
+      I.w_head = s + 1 == P.wcap ? 0 : s + 1;
       I.w_cnt--;
-      lane_admit_one(G, i, I, req, prompt, dhat, tru, emit);
-      lane_refill(P, G, off, i, I);
+      lane_admit_one(P, gw, i, I, req, prompt, dhat, tru, emit);
+      lane_refill(P, gw, off, i, I);
       continue;
     }
     // BinPacking (largest reservation that fits, first wins) or
     // LeastWorkLeft (smallest decode_left that fits, first wins).
     const bool bp = P.batching == RS_BATCHING_BIN_PACKING;
-    int best = -1, bkey = 0, pos = -1, preq = -1;
+    bool found = false;
+    int bkey = 0, pos = -1, preq = -1;
     for (int q = 0; q < I.w_cnt; ++q) {
       int s = I.w_head + q;
       if (s >= P.wcap) s -= P.wcap;
-      const int b = i * G.wstride + s;
-      const int prompt = G.w_prompt[b], dhat = G.w_dhat[b], emit = G.w_emit[b];
+      const int prompt = WP(P, gw, i, s), dhat = WD(P, gw, i, s), emit = WE(P, gw, i, s);
       const int need = reserved_of(prompt, dhat, emit);
       if (I.res + need > P.kv_cap) continue;
       const int key = bp ? -need : (dhat > emit ? dhat - emit : 0);
-      if (best < 0 || key < bkey) { best = 1; bkey = key; pos = q; }
+      if (!found || key < bkey) { found = true; bkey = key; pos = q; }
     }
     int cur = I.o_head;
     for (int q = 0; q < I.o_cnt; ++q) {
@@ -240,51 +247,43 @@ __device__ inline void lane_admit(const KParams& P, const FastGrp& G, long long 
       const int need = reserved_of(prompt, dhat, emit);
       if (I.res + need <= P.kv_cap) {
         const int key = bp ? -need : (dhat > emit ? dhat - emit : 0);
-        if (best < 0 || key < bkey) { best = 1; bkey = key; pos = I.w_cnt + q; preq = cur; }
+        if (!found || key < bkey) { found = true; bkey = key; pos = I.w_cnt + q; preq = cur; }
       }
       cur = (int)P.ov_next[off + cur];
     }
-    if (best < 0) break;
+    if (!found) break;
     if (pos < I.w_cnt) {
       int s = I.w_head + pos;
       if (s >= P.wcap) s -= P.wcap;
-      const int b = i * G.wstride + s;
-      const int req = G.w_req[b], prompt = G.w_prompt[b], dhat = G.w_dhat[b], tru = G.w_true[b],
-                emit = G.w_emit[b];
+      const int req = WQ(P, gw, i, s), prompt = WP(P, gw, i, s), dhat = WD(P, gw, i, s),
+                tru = WT(P, gw, i, s), emit = WE(P, gw, i, s);
       for (int q = pos; q + 1 < I.w_cnt; ++q) {  // erase, order kept
         int s0 = I.w_head + q, s1 = s0 + 1;
         if (s0 >= P.wcap) s0 -= P.wcap;
         if (s1 >= P.wcap) s1 -= P.wcap;
-        const int b0 = i * G.wstride + s0, b1 = i * G.wstride + s1;
-        G.w_req[b0] = G.w_req[b1];
-        G.w_prompt[b0] = G.w_prompt[b1];
-        G.w_dhat[b0] = G.w_dhat[b1];
-        G.w_true[b0] = G.w_true[b1];
-        G.w_emit[b0] = G.w_emit[b1];
+        ring_put(P, gw, i, s0, WQ(P, gw, i, s1), WP(P, gw, i, s1), WD(P, gw, i, s1),
+                 WT(P, gw, i, s1), WE(P, gw, i, s1));
       }
       I.w_cnt--;
-      lane_admit_one(G, i, I, req, prompt, dhat, tru, emit);
-      lane_refill(P, G, off, i, I);
+      lane_admit_one(P, gw, i, I, req, prompt, dhat, tru, emit);
+      lane_refill(P, gw, off, i, I);
     } else {
       const int prompt = P.prompt[off + preq], tru = P.decode[off + preq];
       const int dhat = P.ub[P.bucket[off + preq]], emit = P.ov_emit[off + preq];
       lane_ov_unlink(P, off, I, preq);
-      lane_admit_one(G, i, I, preq, prompt, dhat, tru, emit);
+      lane_admit_one(P, gw, i, I, preq, prompt, dhat, tru, emit);
     }
   }
 }
 
-// Warp-cooperative rescan of instance i's running batch: completions
-// (emitted >= true) are stored and compacted away, then every aggregate is
-// recomputed exactly.  `owner` lane holds the instance; returns to it.
-template <bool NEED_DBC>
-__device__ inline void warp_scan_instance(const KParams& P, const FastGrp& G, long long off, int i,
-                                          int owner, Inst& I, int* dbc_out) {
-  const int l = lane_id();
+// Warp-cooperative rescan of instance i's running batch after a decode
+// step: completions (emitted >= true) are stored and compacted away, then
+// every aggregate is recomputed exactly.  `owner` lane holds the instance.
+__device__ inline void warp_scan_instance(const KParams& P, int gw, long long off, int i,
+                                          int owner, Inst& I, int l) {
   const int D = __shfl_sync(kFull, I.D, owner);
   const int n = __shfl_sync(kFull, I.n, owner);
   const double clock = __shfl_sync(kFull, I.clock, owner);
-  const int base = i * G.R.stride;
   int rq[kMaxRunChunks], pr[kMaxRunChunks], dh[kMaxRunChunks], tr[kMaxRunChunks],
       ky[kMaxRunChunks];
   bool keep[kMaxRunChunks];
@@ -297,11 +296,11 @@ __device__ inline void warp_scan_instance(const KParams& P, const FastGrp& G, lo
     if (k * kWarp < n) {
       bool done = false;
       if (j < n) {
-        rq[k] = G.R.req[base + j];
-        pr[k] = G.R.prompt[base + j];
-        dh[k] = G.R.dhat[base + j];
-        tr[k] = G.R.tru[base + j];
-        ky[k] = G.R.key[base + j];
+        rq[k] = RQ(P, gw, i, j);
+        pr[k] = RP(P, gw, i, j);
+        dh[k] = RD(P, gw, i, j);
+        tr[k] = RT(P, gw, i, j);
+        ky[k] = RK(P, gw, i, j);
         done = D + ky[k] >= tr[k];
         if (done) P.o_completion[off + (rq[k] & kReqMask)] = clock;
         keep[k] = !done;
@@ -310,9 +309,6 @@ __device__ inline void warp_scan_instance(const KParams& P, const FastGrp& G, lo
     }
   }
   int res = 0, kv = 0, dl = 0, tl = 0, tok = 0, nge = 0, nxg = kBig, nxd = kBig;
-  int cnt[RS_MAX_BUCKETS];
-#pragma unroll
-  for (int b = 0; b < RS_MAX_BUCKETS; ++b) cnt[b] = 0;
   int npos = 0;
 #pragma unroll
   for (int k = 0; k < kMaxRunChunks; ++k) {
@@ -320,12 +316,12 @@ __device__ inline void warp_scan_instance(const KParams& P, const FastGrp& G, lo
       if (ncomp) {
         const unsigned km = __ballot_sync(kFull, keep[k]);
         if (keep[k]) {
-          const int d = base + npos + __popc(km & lanemask_lt());
-          G.R.req[d] = rq[k];
-          G.R.prompt[d] = pr[k];
-          G.R.dhat[d] = dh[k];
-          G.R.tru[d] = tr[k];
-          G.R.key[d] = ky[k];
+          const int d = npos + __popc(km & lanemask_lt());
+          RQ(P, gw, i, d) = rq[k];
+          RP(P, gw, i, d) = pr[k];
+          RD(P, gw, i, d) = dh[k];
+          RT(P, gw, i, d) = tr[k];
+          RK(P, gw, i, d) = ky[k];
         }
         npos += __popc(km);
       }
@@ -340,7 +336,6 @@ __device__ inline void warp_scan_instance(const KParams& P, const FastGrp& G, lo
         if (em >= dh[k]) nge++;
         else nxg = min(nxg, dh[k] - ky[k]);
         nxd = min(nxd, tr[k] - ky[k]);
-        if (NEED_DBC) cnt[bucket_of(P.state_edges, P.n_state_edges, d > 0 ? d : 0)]++;
       }
     }
   }
@@ -352,13 +347,6 @@ __device__ inline void warp_scan_instance(const KParams& P, const FastGrp& G, lo
   nge = warp_sum(nge);
   nxg = warp_min(nxg);
   nxd = warp_min(nxd);
-  if (NEED_DBC) {
-#pragma unroll
-    for (int b = 0; b < RS_MAX_BUCKETS; ++b) {
-      const int c = warp_sum(cnt[b]);
-      if (l == b) dbc_out[i * RS_MAX_BUCKETS + b] = c;
-    }
-  }
   __syncwarp();
   if (l == owner) {
     I.n = n - ncomp;
@@ -373,28 +361,54 @@ __device__ inline void warp_scan_instance(const KParams& P, const FastGrp& G, lo
     I.nge = nge;
     I.next_ge = nxg;
     I.next_done = nxd;
-    if (I.ft > I.n) I.ft = I.n;
+    I.ft = I.n;  // every survivor has emitted
   }
 }
 
-// preempt_if_needed (instance.hpp:282-299) by the owning lane; the caller
-// rescans afterwards.  Running is in admission order, so the newest is last.
-__device__ __forceinline__ bool lane_preempt(const KParams& P, const FastGrp& G, long long off,
-                                             int i, Inst& I) {
-  bool any = false;
+// Serial (owner lane) recount of every running aggregate after preemption.
+// No request can complete here: completions were handled this step.
+__device__ inline void lane_recount(const KParams& P, int gw, int i, Inst& I) {
+  int res = 0, kv = 0, dl = 0, tl = 0, tok = 0, nge = 0, nxg = kBig, nxd = kBig;
+  for (int j = 0; j < I.n; ++j) {
+    const int pr = RP(P, gw, i, j), dh = RD(P, gw, i, j), tr = RT(P, gw, i, j),
+              ky = RK(P, gw, i, j);
+    const int em = I.D + ky;
+    res += reserved_of(pr, dh, em);
+    kv += pr + em;
+    dl += dh > em ? dh - em : 0;
+    tl += tr - em;
+    tok += pr + em;
+    if (em >= dh) nge++;
+    else nxg = min(nxg, dh - ky);
+    nxd = min(nxd, tr - ky);
+  }
+  I.res = res;
+  I.kv = kv;
+  I.dleft = dl;
+  I.tleft = tl;
+  I.tok = tok;
+  I.nge = nge;
+  I.next_ge = nxg;
+  I.next_done = nxd;
+}
+
+// preempt_if_needed (instance.hpp:282-299) by the owning lane.  Running is
+// in admission order, so the newest admission is last; all prompts are
+// prefilled at a step boundary.
+__device__ __forceinline__ void lane_preempt(const KParams& P, int gw, long long off, int i,
+                                             Inst& I) {
   while (I.kv > P.kv_cap && I.n > 1) {
-    const int b = i * G.R.stride + I.n - 1;
-    const int req = G.R.req[b] & kReqMask, prompt = G.R.prompt[b], dhat = G.R.dhat[b],
-              tru = G.R.tru[b];
-    const int emit = I.D + G.R.key[b];
-    I.kv -= prompt + emit;  // all prompts are prefilled at a step boundary
+    const int j = I.n - 1;
+    const int req = RQ(P, gw, i, j) & kReqMask, prompt = RP(P, gw, i, j),
+              dhat = RD(P, gw, i, j), tru = RT(P, gw, i, j);
+    const int emit = I.D + RK(P, gw, i, j);
+    I.kv -= prompt + emit;
     I.n--;
     P.o_preempt[off + req] += 1;
-    lane_push_front(P, G, off, i, I, req, prompt, dhat, tru, emit);
-    any = true;
+    lane_push_front(P, gw, off, i, I, req, prompt, dhat, tru, emit);
   }
   if (I.ft > I.n) I.ft = I.n;
-  return any;
+  lane_recount(P, gw, i, I);
 }
 
 }  // namespace rs

@@ -7,10 +7,18 @@ namespace rs {
 
 // InstanceFeatures (instance.hpp:317-360) of the lane's instance at a tick
 // boundary, from the maintained aggregates.  At a step boundary every
-// admitted prompt has been prefilled, so running prompt-bucket counts and
-// pending running prompt tokens are zero.
-__device__ __forceinline__ Feat feat_of(const Inst& I) {
-  Feat f;
+// admitted prompt has been prefilled (whole-prompt prefill), so running
+// prompt-bucket counts and pending running prompt tokens are zero.
+struct FeatI {  // 32-bit InstanceFeatures subset (fast kernel)
+  int res, pend, dleft, tleft, tok, cnt, kv, nrun, mind;
+};
+
+__device__ __forceinline__ bool can_accept(const KParams& P, const FeatI& f, int need) {
+  return P.kv_cap - f.res >= need && f.cnt < P.max_batch;  // policies.hpp:44-48
+}
+
+__device__ __forceinline__ FeatI feat_of(const Inst& I) {
+  FeatI f;
   f.res = I.res + I.resw;
   f.pend = I.pend + I.pendw;
   f.dleft = I.dleft + I.dlw;
@@ -23,18 +31,28 @@ __device__ __forceinline__ Feat feat_of(const Inst& I) {
   return f;
 }
 
+// Lowest lane (< width) holding the minimal key among valid lanes; all valid
+// lanes lie below `width` (a power of two), so log2(width) butterfly rounds.
+__device__ __forceinline__ int argmin_narrow(unsigned long long key, bool valid, int width) {
+  unsigned long long k = valid ? key : ~0ull;
+  for (int o = width >> 1; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(kFull, k, o);
+    k = w < k ? w : k;
+  }
+  const unsigned ok = __ballot_sync(kFull, valid && key == k);
+  return ok ? __ffs(ok) - 1 : -1;
+}
+
 // decode-bucket counts (state edges) of instance i's running batch
-__device__ inline void warp_dbc(const KParams& P, const FastGrp& G, int i, int owner,
-                                const Inst& I, int* dbc) {
-  const int l = lane_id();
+__device__ inline void warp_dbc(const KParams& P, int gw, int i, int owner, const Inst& I, int* dbc,
+                                int l) {
   const int D = __shfl_sync(kFull, I.D, owner);
   const int n = __shfl_sync(kFull, I.n, owner);
-  const int base = i * G.R.stride;
   int cnt[RS_MAX_BUCKETS];
 #pragma unroll
   for (int b = 0; b < RS_MAX_BUCKETS; ++b) cnt[b] = 0;
   for (int j = l; j < n; j += kWarp) {
-    const int d = G.R.dhat[base + j] - (D + G.R.key[base + j]);
+    const int d = RD(P, gw, i, j) - (D + RK(P, gw, i, j));
     cnt[bucket_of(P.state_edges, P.n_state_edges, d > 0 ? d : 0)]++;
   }
 #pragma unroll
@@ -45,18 +63,17 @@ __device__ inline void warp_dbc(const KParams& P, const FastGrp& G, int i, int o
 }
 
 template <int POL, int G>
-__device__ inline int decide_fast(const KParams& P, const FastGrp& FG, const MlpView& M,
-                                  Replay& R, const Inst (&S)[G], bool has_head, const Rec& hr,
-                                  int hb, int* dbc) {
+__device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Replay& R,
+                                  const Inst (&S)[G], bool has_head, const Rec& hr, int hb,
+                                  char* gbase, int l) {
   const int m = P.m;
-  const int l = lane_id();
   const int need = reserved_of(hr.prompt, hr.dhat, 0);
   if (POL == RS_POLICY_ROUND_ROBIN || POL == RS_POLICY_DEDICATED_SMALL_LARGE) {
     if (!has_head) return m;
     int t;
-    if (POL == RS_POLICY_ROUND_ROBIN) {
+    if (POL == RS_POLICY_ROUND_ROBIN) {  // policies.hpp:50-69
       t = (int)(R.rr_next % (unsigned long long)m);
-    } else {
+    } else {  // policies.hpp:73-104
       if (m < 2 || hr.dhat >= P.dsl_cutoff) t = 0;
       else t = 1 + (int)(R.dsl_next % (unsigned long long)(m - 1));
     }
@@ -69,7 +86,7 @@ __device__ inline int decide_fast(const KParams& P, const FastGrp& FG, const Mlp
     if (POL == RS_POLICY_ROUND_ROBIN) R.rr_next++;
     else if (m >= 2 && t >= 1) R.dsl_next++;
     return t;
-  } else if (POL == RS_POLICY_EARLIEST_AVAILABLE) {
+  } else if (POL == RS_POLICY_EARLIEST_AVAILABLE) {  // policies.hpp:214-228
     if (!has_head) return m;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -79,7 +96,7 @@ __device__ inline int decide_fast(const KParams& P, const FastGrp& FG, const Mlp
       if (b) return g * kWarp + __ffs(b) - 1;
     }
     return m;
-  } else if (POL == RS_POLICY_MAX_CAPACITY) {
+  } else if (POL == RS_POLICY_MAX_CAPACITY) {  // policies.hpp:150-170
     if (!has_head || R.clock < R.mc_next) return m;
     unsigned long long bk = 0;
     int bi = -1;
@@ -102,25 +119,37 @@ __device__ inline int decide_fast(const KParams& P, const FastGrp& FG, const Mlp
     if (!ok) return m;
     R.mc_next = __dadd_rn(R.clock, 1.0);
     return bi;
-  } else if (POL == RS_POLICY_RL) {
-    double* x = FG.rlx;
+  } else if (POL == RS_POLICY_RL) {  // RlPolicy + encode_state (env.hpp:88-113)
+    double* x = reinterpret_cast<double*>(gbase + P.off_rlx);
     const int nsb = P.n_state_edges;
     const int per = 3 + nsb;
-    for (int i = 0; i < m; ++i) {  // decode-bucket counts, whole warp per instance
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (i / kWarp == g) warp_dbc(P, FG, i, i & (kWarp - 1), S[g], dbc);
-    }
-    __syncwarp();
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int i = g * kWarp + l;
       if (i < m) {
-        const Feat f = feat_of(S[g]);
+        const FeatI f = feat_of(S[g]);
         double* xi = x + i * per;
-        xi[0] = __ddiv_rn((double)f.pend, (double)P.kv_cap);
-        for (int b = 0; b < nsb; ++b)
-          xi[1 + b] = __ddiv_rn((double)dbc[i * RS_MAX_BUCKETS + b], (double)P.max_batch);
+        xi[0] = div_exact((double)f.pend, (double)P.kv_cap, P.inv_kv, P.kv_pow2);
+        // decode-bucket counts of the running batch (every running request
+        // is in its decode phase at a tick boundary), counted by the owner
+        // lane: cge[b] = #requests with decode_left >= state edge b
+        int cge[RS_MAX_BUCKETS + 1];
+#pragma unroll
+        for (int b = 0; b < RS_MAX_BUCKETS; ++b) cge[b] = 0;
+        for (int j = 0; j < S[g].n; ++j) {
+          int d = RD(P, gw, i, j) - (S[g].D + RK(P, gw, i, j));
+          d = d > 0 ? d : 0;
+#pragma unroll
+          for (int b = 1; b < RS_MAX_BUCKETS; ++b)
+            if (b < nsb) cge[b] += d >= P.state_edges[b];
+        }
+#pragma unroll
+        for (int b = 0; b < RS_MAX_BUCKETS; ++b) {
+          if (b >= nsb) break;
+          const int hi = b + 1 < nsb ? cge[b + 1] : 0;
+          const int c = (b == 0 ? S[g].n : cge[b]) - hi;
+          xi[1 + b] = div_exact((double)c, (double)P.max_batch, P.inv_mb, P.mb_pow2);
+        }
         xi[1 + nsb] = round2(capacity_of(P, f.kv));
         const double that = f.nrun == 0 ? 0.0 : __dmul_rn(P.dtb, (double)f.mind);
         xi[2 + nsb] = round2(that);
@@ -134,18 +163,24 @@ __device__ inline int decide_fast(const KParams& P, const FastGrp& FG, const Mlp
     }
     __syncwarp();
     const int na = P.rl_dims[P.rl_layers];
-    if (P.rl_eps > 0.0) {
-      const double u = u01(rng_draw(FG.rng, R));
+    if (P.rl_eps > 0.0) {  // DqnAgent::act (dqn.hpp:92-99)
+      unsigned long long* rng = reinterpret_cast<unsigned long long*>(gbase + P.off_rng);
+      const double u = u01(rng_draw(rng, R, l));
       if (u < P.rl_eps) {
-        const double v = __dmul_rn(u01(rng_draw(FG.rng, R)), (double)na);
+        const double v = __dmul_rn(u01(rng_draw(rng, R, l)), (double)na);
         const unsigned long long k = (unsigned long long)v;
         return (int)(k < (unsigned long long)na ? k : (unsigned long long)na - 1);
       }
     }
+    if (!P.rl_wt_global) {  // staged weights: LDS-only forward over nonzero inputs
+      const int xd = (gw >> 1) + (P.off_rlx >> 3);
+      return mlp_forward_smem(P.rl_dims, P.rl_woff, P.rl_boff, P.rl_layers, xd,
+                              xd + P.rl_dims[0], xd + P.rl_dims[0] + P.rl_maxw, l);
+    }
     double* h0 = x + M.dims[0];
     double* h1 = h0 + P.rl_maxw;
-    return mlp_forward_warp(M, x, h0, h1, nullptr);
-  } else {
+    return mlp_forward_warp(M, x, h0, h1, nullptr, l);
+  } else {  // argmin policies
     if (!has_head) return m;
     unsigned long long bk = ~0ull;
     int bi = -1;
@@ -155,7 +190,7 @@ __device__ inline int decide_fast(const KParams& P, const FastGrp& FG, const Mlp
       bool v = i < m;
       unsigned long long k = ~0ull;
       if (v) {
-        const Feat f = feat_of(S[g]);
+        const FeatI f = feat_of(S[g]);
         if (POL == RS_POLICY_DECODE_BALANCER) {  // policies.hpp:108-127
           v = can_accept(P, f, need);
           k = (unsigned long long)f.tleft;
@@ -166,20 +201,21 @@ __device__ inline int decide_fast(const KParams& P, const FastGrp& FG, const Mlp
                                     __dmul_rn((double)f.dleft, P.dtb)));
         } else {  // workload_aware, SURVEY.md Appendix B
           v = can_accept(P, f, need);
-          const long long p = hr.prompt, d = hr.dhat;
+          const int p = hr.prompt, d = hr.dhat;
           const double avail = __dmul_rn(P.dtb, (double)f.dleft);
           const double pcost = __dmul_rn(P.tpp, (double)(f.pend + p));
           const double pi = (double)p;
           const double lead = P.prompt_exp == 2 ? __dmul_rn(pi, pi) : pi;
           const double t_p = __dmul_rn(P.grad1, __dadd_rn(lead, (double)f.tok));
-          const double r_p = t_p <= P.eps_s ? 1.0 : __dsub_rn(1.0, __ddiv_rn(t_p, P.eps_s));
+          const double r_p =
+              t_p <= P.eps_s ? 1.0 : __dsub_rn(1.0, div_exact(t_p, P.eps_s, P.inv_eps, P.eps_pow2));
           const double r_d = __dmul_rn(-P.grad2, (double)(f.tok + p + d));
           const double mix = __dadd_rn(__dmul_rn(P.alpha, r_p),
                                        __dmul_rn(__dsub_rn(1.0, P.alpha), r_d));
           k = ordered_key(__dsub_rn(__dadd_rn(avail, pcost), __dmul_rn(P.eps_s, mix)));
         }
       }
-      const int a = warp_argmin_key(k, v);
+      const int a = G == 1 ? argmin_narrow(k, v, P.mwidth) : warp_argmin_key(k, v);
       if (a >= 0) {
         const unsigned long long ka = __shfl_sync(kFull, k, a);
         if (bi < 0 || ka < bk) { bk = ka; bi = g * kWarp + a; }
@@ -192,16 +228,17 @@ __device__ inline int decide_fast(const KParams& P, const FastGrp& FG, const Mlp
 
 // Returns true when the replay must be re-run instance-sequentially.
 template <int POL, int G>
-__device__ bool run_replay_fast(const KParams& P, const FastGrp& FG, const MlpView& M, int r,
-                                bool seq, int* dbc) {
-  const int l = lane_id();
+__device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const MlpView& M, int r,
+                                bool seq, int l) {
   Replay R;
   R.off = P.offsets[r];
   R.n = (int)(P.offsets[r + 1] - R.off);
   const int m = P.m;
   const long long off = R.off;
+  int* front = reinterpret_cast<int*>(gbase + P.off_front);
 
   bool bad = false;
+  int vmax = 0;
   for (int j = l; j < R.n; j += kWarp) {
     const long long g = off + j;
     P.o_instance[g] = -1;
@@ -213,8 +250,13 @@ __device__ bool run_replay_fast(const KParams& P, const FastGrp& FG, const MlpVi
     const int p = P.prompt[g], d = P.decode[g];
     if (p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens) bad = true;
     if (j > 0 && P.arrival[g] < P.arrival[g - 1]) bad = true;
+    const int v = p + (d > P.ub_max ? d : P.ub_max);
+    vmax = v > vmax ? v : vmax;
   }
   bad = __any_sync(kFull, bad);
+  // 32-bit aggregate guard: every per-instance token sum is bounded by
+  // N x max(prompt + max(decode, bucket bound)) (+ the running batch)
+  const bool too_big = (long long)R.n * warp_max(vmax) > (1ll << 30);
   Inst S[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) inst_init(S[g]);
@@ -235,37 +277,40 @@ __device__ bool run_replay_fast(const KParams& P, const FastGrp& FG, const MlpVi
   R.h_base = -2 * kWarp;
   R.h_prompt = R.h_true = R.h_bucket = 0;
   if (POL == RS_POLICY_RL && P.rl_eps > 0.0)
-    mt_seed_warp(FG.rng, P.policy_seed ? P.policy_seed[r] : 0ull);
+    mt_seed_warp(reinterpret_cast<unsigned long long*>(gbase + P.off_rng),
+                 P.policy_seed ? P.policy_seed[r] : 0ull, l);
   __syncwarp();
-  load_arrival_window(P, R);
+  load_arrival_window(P, R, l);
   if (bad) R.status = RS_REPLAY_INVALID_TRACE;
-  else inject(P, R);
+  else if (too_big) R.status = RS_REPLAY_CAPACITY;
+  else inject(P, R, l);
 
   while (R.status == RS_REPLAY_FINISHED && R.completed != R.n && R.tick < P.max_ticks) {
     if (POL == RS_POLICY_MIN_MIN && queue_len<POL>(R) > 0) {
-      if (!minmin_pick(P, FG.front, R)) { R.status = RS_REPLAY_CAPACITY; break; }
+      if (!minmin_pick(P, front, R, l)) { R.status = RS_REPLAY_CAPACITY; break; }
     }
     const bool has_head = queue_len<POL>(R) > 0;
     Rec hr;
     int hb = 0;
-    if (has_head) hr = head_rec<POL>(P, FG.front, R, &hb);
+    if (has_head) hr = head_rec<POL>(P, front, R, &hb, l);
     else hr.req = hr.prompt = hr.dhat = hr.tru = hr.emit = 0;
-    const int action = decide_fast<POL, G>(P, FG, M, R, S, has_head, hr, hb, dbc);
+    const int action = decide_fast<POL, G>(P, gw, M, R, S, has_head, hr, hb, gbase, l);
     R.hash = hash_action(R.hash, action);
     if (action < 0 || action > m) { R.status = RS_REPLAY_BAD_ACTION; break; }
     const double t1 = __dadd_rn(R.clock, P.delta_t);
+    int wdelta = 0;  // this lane's waiting-count change over the tick
     if (action < m && has_head) {
       if ((long long)hr.prompt + hr.tru > P.kv_cap) {
-        R.infeasible++;
+        R.infeasible++;  // env.hpp:262-267: flagged, stays queued
       } else {
         if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) {
           if (l == 0)
-            for (int k = 0; k + 1 < R.nfront; ++k) FG.front[k] = FG.front[k + 1];
+            for (int k = 0; k + 1 < R.nfront; ++k) front[k] = front[k + 1];
           __syncwarp();
           R.nfront--;
         } else {
           R.qhead++;
-          if (POL == RS_POLICY_MIN_MIN) mm_skip_removed(P, R);
+          if (POL == RS_POLICY_MIN_MIN) mm_skip_removed(P, R, l);
         }
         if (l == 0) {
           P.o_routed[off + hr.req] = R.clock;
@@ -274,12 +319,14 @@ __device__ bool run_replay_fast(const KParams& P, const FastGrp& FG, const MlpVi
         R.routed++;
 #pragma unroll
         for (int g = 0; g < G; ++g)
-          if (g * kWarp + l == action) lane_enqueue(P, FG, off, action, S[g], hr, R.clock);
+          if (g * kWarp + l == action) {
+            lane_enqueue(P, gw, off, action, S[g], hr, R.clock);
+            wdelta++;
+          }
       }
     }
 
     // ---- run_until(t1) for every instance (env.hpp:277-287) -----------
-    int err = kBig;
     for (;;) {
       bool act[G];
       unsigned any = 0;
@@ -291,115 +338,131 @@ __device__ bool run_replay_fast(const KParams& P, const FastGrp& FG, const MlpVi
           if (S[g].n > 0 || S[g].w_cnt > 0) act[g] = true;
           else S[g].clock = t1;  // idle instance skips ahead (instance.hpp:309)
         }
-        any |= __ballot_sync(kFull, act[g]) ? (1u << g) : 0u;
+        any |= act[g] ? (1u << g) : 0u;
       }
-      if (!any) break;
+      const unsigned am = __ballot_sync(kFull, any != 0);
+      if (!am) break;
       if (seq) {  // only the lowest-index instance that still has work
-        const int g0 = __ffs(any) - 1;
+        int g0 = G;
+#pragma unroll
+        for (int g = G - 1; g >= 0; --g)
+          if (__ballot_sync(kFull, act[g])) g0 = g;
         const unsigned lm = __ballot_sync(kFull, act[g0 < G ? g0 : 0]);
 #pragma unroll
         for (int g = 0; g < G; ++g) act[g] = act[g] && g == g0 && l == __ffs(lm) - 1;
       }
-      bool first[G], dec[G], scan[G];
+      bool ev = false;
+      unsigned evg = 0;
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        first[g] = dec[g] = scan[g] = false;
         if (!act[g]) continue;
         Inst& I = S[g];
         const int i = g * kWarp + l;
-        if (I.w_cnt > 0 && I.n < P.max_batch) lane_admit(P, FG, off, i, I);
+        if (I.w_cnt > 0 && I.n < P.max_batch) {
+          const int w0 = I.w_cnt + I.o_cnt;
+          lane_admit(P, gw, off, i, I);
+          wdelta += I.w_cnt + I.o_cnt - w0;
+        }
         if (I.n == 0) {  // logic_error, instance.hpp:209-211
-          err = min(err, i);
-          act[g] = false;
+          ev = true;
+          evg |= 1u << g;
           continue;
         }
-        if (I.npf > 0) {  // whole-prompt prefill, co-running decodes stall
-          I.clock = __dadd_rn(I.clock, __dadd_rn(__dadd_rn(P.intercept, __dmul_rn(P.tpp, (double)I.pend)),
+        if (I.npf > 0) {  // whole-prompt prefill; co-running decodes stall
+          I.clock = __dadd_rn(I.clock, __dadd_rn(__dadd_rn(P.intercept,
+                                                           __dmul_rn(P.tpp, (double)I.pend)),
                                                  __dmul_rn(P.dpt, (double)I.kv)));
           I.kv += I.pend;
           I.pend = 0;
           I.npf = 0;
+          if (I.kv > P.kv_cap && I.n > 1) { ev = true; evg |= 1u << g; }
         } else {  // every running request emits one token
           const int n = I.n;
-          I.clock = __dadd_rn(I.clock, __dadd_rn(P.dtb, __dmul_rn(P.dpt, (double)n)));
+          if (n != I.el_n) {
+            I.dec_el = __dadd_rn(P.dtb, __dmul_rn(P.dpt, (double)n));
+            I.el_n = n;
+          }
+          I.clock = __dadd_rn(I.clock, I.dec_el);
           I.D++;
           I.kv += n;
           I.tleft -= n;
           I.tok += n;
           I.res += I.nge;
           I.dleft -= n - I.nge;
-          dec[g] = true;
-          first[g] = I.ft < n;
-          scan[g] = I.D >= I.next_done || I.D >= I.next_ge;
+          if (I.ft < n) {  // first tokens of requests admitted since the last decode
+            for (int j = I.ft; j < n; ++j) {
+              const int q = RQ(P, gw, i, j);
+              if (q & kFresh) P.o_first[off + (q & kReqMask)] = I.clock;
+            }
+            I.ft = n;
+          }
+          if (I.D >= I.next_done || I.D >= I.next_ge || (I.kv > P.kv_cap && n > 1)) {
+            ev = true;
+            evg |= 1u << g;
+          }
         }
       }
-      if (__any_sync(kFull, err != kBig)) {
+      unsigned evm = __ballot_sync(kFull, ev);
+      if (!evm) continue;
+      // ---- events (whole warp): errors, completion scans, preemption ----
+      {
+        int err = kBig;
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+          if ((evg >> g) & 1u)
+            if (S[g].n == 0) err = min(err, g * kWarp + l);
         err = warp_min(err);
-        if (!seq) return true;  // exact stop point needs index order: re-run
-        R.status = RS_REPLAY_NOT_ADMISSIBLE;
-        R.err_inst = err;
-        break;
-      }
-      // first tokens of the requests admitted since the last decode step
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        if (!first[g]) continue;
-        const Inst& I = S[g];
-        const int base = (g * kWarp + l) * FG.R.stride;
-        for (int j = I.ft; j < I.n; ++j) {
-          const int q = FG.R.req[base + j];
-          if (q & kFresh) P.o_first[off + (q & kReqMask)] = I.clock;
+        if (err != kBig) {
+          if (!seq) return true;  // exact stop point needs index order: re-run
+          R.status = RS_REPLAY_NOT_ADMISSIBLE;
+          R.err_inst = err;
+          break;
         }
       }
-      // completion / estimate-reached events: whole warp per instance
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        unsigned sm = __ballot_sync(kFull, scan[g]);
+        const bool mine = (evg >> g) & 1u;
+        const bool sc = mine && (S[g].D >= S[g].next_done || S[g].D >= S[g].next_ge) &&
+                        S[g].npf == 0 && S[g].el_n == S[g].n;
+        unsigned sm = __ballot_sync(kFull, sc);
         while (sm) {
           const int owner = __ffs(sm) - 1;
           sm &= sm - 1;
-          warp_scan_instance<false>(P, FG, off, g * kWarp + owner, owner, S[g], dbc);
+          warp_scan_instance(P, gw, off, g * kWarp + owner, owner, S[g], l);
         }
-        if (dec[g]) S[g].ft = S[g].n;
-      }
-      // preemption (rare): owner lane evicts, whole warp rescans
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        bool pre = false;
-        if (act[g] && S[g].kv > P.kv_cap && S[g].n > 1)
-          pre = lane_preempt(P, FG, off, g * kWarp + l, S[g]);
-        unsigned pm = __ballot_sync(kFull, pre);
-        while (pm) {
-          const int owner = __ffs(pm) - 1;
-          pm &= pm - 1;
-          warp_scan_instance<false>(P, FG, off, g * kWarp + owner, owner, S[g], dbc);
+        if (mine && S[g].kv > P.kv_cap && S[g].n > 1) {
+          const int w0 = S[g].w_cnt + S[g].o_cnt;
+          lane_preempt(P, gw, off, g * kWarp + l, S[g]);
+          wdelta += S[g].w_cnt + S[g].o_cnt - w0;
         }
       }
     }
     if (R.status != RS_REPLAY_FINISHED) break;
-    int comps = 0, wait = 0;
+    int comps = 0;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       comps += S[g].comps;
       S[g].comps = 0;
-      if (g * kWarp + l < m) wait += S[g].w_cnt + S[g].o_cnt;
     }
-    R.completed += warp_sum(comps);
+    // one reduction: completions (low 16 bits) + biased waiting deltas
+    const unsigned packed = warp_sum((int)((unsigned)comps | ((unsigned)(wdelta + 1024) << 16)));
+    R.completed += (int)(packed & 0xffffu);
+    R.total_wait += (int)(packed >> 16) - kWarp * 1024;
     R.clock = t1;
-    inject(P, R);
+    inject(P, R, l);
     R.tick++;
     R.sum_q += queue_len<POL>(R);
-    R.sum_w += warp_sum(wait);
+    R.sum_w += R.total_wait;
   }
   if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
-  write_replay_stats(P, R, r);
+  write_replay_stats(P, R, r, l);
   return false;
 }
 
 template <int POL, int G>
 __global__ void __launch_bounds__(256) replay_fast_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) char smem[];
-  const int w = threadIdx.x / kWarp;
+  const int l = opaque_lane();
   MlpView M;
   M.layers = P.rl_layers;
   M.dims = P.rl_dims;
@@ -408,20 +471,25 @@ __global__ void __launch_bounds__(256) replay_fast_kernel(const __grid_constant_
   M.w = reinterpret_cast<const double*>(smem);
   int groups_off = 0;
   if (POL == RS_POLICY_RL) {
-    mlp_stage_weights(P.rl_w, P.rl_layers, P.rl_dims, P.rl_woff, P.rl_boff,
-                      reinterpret_cast<double*>(smem));
-    groups_off = P.smem_weights_bytes;
+    if (P.rl_wt_global) {  // too big for shared memory: transposed copy in L2
+      M.w = P.rl_wt_global;
+    } else {
+      mlp_stage_weights(P.rl_w, P.rl_layers, P.rl_dims, P.rl_woff, P.rl_boff,
+                        reinterpret_cast<double*>(smem));
+      groups_off = P.smem_weights_bytes;
+    }
   }
-  char* gbase = smem + groups_off + (size_t)w * P.smem_group_bytes;
-  const FastGrp FG = make_fast_grp(P, gbase);
-  int* dbc = reinterpret_cast<int*>(gbase + P.off_dbc);
+  int gbyte = groups_off + (int)(threadIdx.x / kWarp) * P.smem_group_bytes;
+  asm volatile("" : "+r"(gbyte));  // keep the group base in a register
+  char* gbase = smem + gbyte;
+  const int gw = gbyte >> 2;
   for (;;) {
     int r = 0;
-    if (lane_id() == 0) r = atomicAdd(P.work_counter, 1);
+    if (l == 0) r = atomicAdd(P.work_counter, 1);
     r = __shfl_sync(kFull, r, 0);
     if (r >= P.num_replays) break;
-    if (run_replay_fast<POL, G>(P, FG, M, r, false, dbc))
-      run_replay_fast<POL, G>(P, FG, M, r, true, dbc);
+    if (run_replay_fast<POL, G>(P, gw, gbase, M, r, false, l))
+      run_replay_fast<POL, G>(P, gw, gbase, M, r, true, l);
   }
 }
 

@@ -64,6 +64,7 @@ struct MlpKParams {
   int dims[RS_MAX_LAYERS + 1];
   int woff[RS_MAX_LAYERS], boff[RS_MAX_LAYERS];
   int maxw, weights_doubles;
+  const double* wt_global;  // transposed weights in global memory, or null (stage in smem)
   const double* params;
   const double* states;
   int batch;
@@ -76,17 +77,21 @@ constexpr int kMlpWarps = 4;
 __global__ void __launch_bounds__(rs::kWarp * kMlpWarps) mlp_kernel(const __grid_constant__ MlpKParams P) {
   extern __shared__ __align__(16) char smem[];
   double* w = reinterpret_cast<double*>(smem);
-  rs::mlp_stage_weights(P.params, P.layers, P.dims, P.woff, P.boff, w);
+  double* scratch = w;
+  if (!P.wt_global) {
+    rs::mlp_stage_weights(P.params, P.layers, P.dims, P.woff, P.boff, w);
+    scratch = w + P.weights_doubles;
+  }
   const int wid = threadIdx.x / rs::kWarp;
-  double* x = w + P.weights_doubles + (size_t)wid * (P.dims[0] + 2 * P.maxw);
+  double* x = scratch + (size_t)wid * (P.dims[0] + 2 * P.maxw);
   double* h0 = x + P.dims[0];
   double* h1 = h0 + P.maxw;
-  rs::MlpView M{P.layers, P.dims, P.woff, P.boff, w};
+  rs::MlpView M{P.layers, P.dims, P.woff, P.boff, P.wt_global ? P.wt_global : w};
   const int dout = P.dims[P.layers];
   for (int b = blockIdx.x * kMlpWarps + wid; b < P.batch; b += gridDim.x * kMlpWarps) {
     for (int i = rs::lane_id(); i < P.dims[0]; i += rs::kWarp) x[i] = P.states[(size_t)b * P.dims[0] + i];
     __syncwarp();
-    const int a = rs::mlp_forward_warp(M, x, h0, h1, P.q + (size_t)b * dout);
+    const int a = rs::mlp_forward_warp(M, x, h0, h1, P.q + (size_t)b * dout, rs::lane_id());
     if (rs::lane_id() == 0) P.greedy[b] = a;
     __syncwarp();
   }
@@ -260,6 +265,7 @@ rs_status rs_mlp_forward_host(const rs_batch_cfg* cfg, const double* states, int
   const size_t o_x = o; o += al((size_t)batch * d0 * 8);
   const size_t o_q = o; o += al((size_t)batch * dout * 8);
   const size_t o_g = o; o += al((size_t)batch * 4);
+  const size_t o_t = o; o += al(w * 8);  // transposed copy (global-weights mode)
   DeviceCache& dc = g_cache[device];
   std::lock_guard<std::mutex> lock(dc.mu);
   char* b = nullptr;
@@ -273,7 +279,23 @@ rs_status rs_mlp_forward_host(const rs_batch_cfg* cfg, const double* states, int
   P.batch = batch;
   P.q = reinterpret_cast<double*>(b + o_q);
   P.greedy = reinterpret_cast<int*>(b + o_g);
-  const int smem = (int)(w * 8 + (size_t)kMlpWarps * (d0 + 2 * P.maxw) * 8);
+  int smem = (int)(w * 8 + (size_t)kMlpWarps * (d0 + 2 * P.maxw) * 8);
+  if (smem > 200 * 1024) {  // too large to stage: transposed copy in global memory
+    rs::MlpTransposeArgs ta;
+    ta.params = P.params;
+    ta.layers = P.layers;
+    for (int l = 0; l <= RS_MAX_LAYERS; ++l) ta.dims[l] = P.dims[l];
+    for (int l = 0; l < RS_MAX_LAYERS; ++l) {
+      ta.woff[l] = P.woff[l];
+      ta.boff[l] = P.boff[l];
+    }
+    ta.out = reinterpret_cast<double*>(b + o_t);
+    ta.count = w;
+    rs::mlp_transpose_kernel<0><<<(unsigned)((w + 255) / 256), 256, 0, st>>>(ta);
+    RS_CUDA2(cudaGetLastError());
+    P.wt_global = ta.out;
+    smem = (int)((size_t)kMlpWarps * (d0 + 2 * P.maxw) * 8);
+  }
   RS_CUDA2(cudaFuncSetAttribute(mlp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const int grid = std::min(1024, (batch + kMlpWarps - 1) / kMlpWarps);
   mlp_kernel<<<grid, rs::kWarp * kMlpWarps, smem, st>>>(P);

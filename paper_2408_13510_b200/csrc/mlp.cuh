@@ -34,8 +34,7 @@ struct MlpView {
 // warp.  h0/h1: shared scratch of max width.  Writes the final layer to
 // `q_out` (may be nullptr) and returns argmax_action (dqn.hpp:82-90).
 __device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double* h0,
-                                       double* h1, double* q_out) {
-  const int l = lane_id();
+                                       double* h1, double* q_out, int l) {
   const double* cur = x;
   unsigned long long best_key = 0;
   int best_idx = 0x7fffffff;
@@ -87,6 +86,127 @@ __device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double
   const unsigned long long gmax = warp_max_u64(have ? best_key : 0ull);
   const int cand = (have && best_key == gmax) ? best_idx : 0x7fffffff;
   return warp_min(cand);
+}
+
+extern __shared__ __align__(16) double rs_smd[];
+
+// widest layer the shared-memory forward handles (wider nets: global path)
+constexpr int kMlpMaskWords = 4;
+constexpr int kMlpSmemMaxWidth = kMlpMaskWords * kWarp;
+
+// Same forward with weights staged in shared memory at double index 0 and
+// x / h0 / h1 at double indices xd / h0d / h1d: every access is an LDS.64
+// with 32-bit addressing, and only the nonzero inputs are visited, in
+// ascending index order (ballot bitmasks), so each output still accumulates
+// acc = b; acc += w*x over i = 0..ni-1 with the zero terms omitted exactly
+// as in mlp_forward_warp.
+__device__ inline int mlp_forward_smem(const int* dims, const int* woff, const int* boff, int layers,
+                                       int xd, int h0d, int h1d, int l) {
+  int cur = xd;
+  // nonzero masks of the current input vector (<= 32 * kMlpMaskWords entries)
+  unsigned nz[kMlpMaskWords];
+  const int n0 = dims[0];
+#pragma unroll
+  for (int c = 0; c < kMlpMaskWords; ++c) {
+    const int i = c * kWarp + l;
+    nz[c] = c * kWarp < n0 ? __ballot_sync(kFull, i < n0 && rs_smd[cur + i] != 0.0) : 0u;
+  }
+  unsigned long long best_key = 0;
+  int best_idx = 0x7fffffff;
+  bool have = false;
+  for (int layer = 0; layer < layers; ++layer) {
+    const int ni = dims[layer], no = dims[layer + 1];
+    const int wt = woff[layer], bs = boff[layer];
+    const bool last = layer + 1 == layers;
+    const int dst = (layer & 1) ? h1d : h0d;
+    unsigned nn[kMlpMaskWords];
+#pragma unroll
+    for (int c = 0; c < kMlpMaskWords; ++c) nn[c] = 0u;
+    for (int ob = 0; ob < no; ob += 2 * kWarp) {
+      const int o0 = ob + l, o1 = ob + kWarp + l;
+      const bool v0 = o0 < no, v1 = o1 < no;
+      double a0 = v0 ? rs_smd[bs + o0] : 0.0;
+      double a1 = v1 ? rs_smd[bs + o1] : 0.0;
+      const int c0 = v0 ? o0 : 0, c1 = v1 ? o1 : 0;
+#pragma unroll
+      for (int c = 0; c < kMlpMaskWords; ++c) {
+        if (c * kWarp >= ni) break;
+        for (unsigned msk = nz[c]; msk; msk &= msk - 1) {
+          const int i = c * kWarp + __ffs(msk) - 1;
+          const double xi = rs_smd[cur + i];
+          const int row = wt + i * no;
+          a0 = __dadd_rn(a0, __dmul_rn(rs_smd[row + c0], xi));
+          a1 = __dadd_rn(a1, __dmul_rn(rs_smd[row + c1], xi));
+        }
+      }
+      if (!last) {
+        const double r0 = a0 > 0.0 ? a0 : 0.0, r1 = a1 > 0.0 ? a1 : 0.0;
+        if (v0) rs_smd[dst + o0] = r0;
+        if (v1) rs_smd[dst + o1] = r1;
+        const unsigned b0 = __ballot_sync(kFull, v0 && r0 != 0.0);
+        const unsigned b1 = __ballot_sync(kFull, v1 && r1 != 0.0);
+#pragma unroll
+        for (int c = 0; c < kMlpMaskWords; ++c) {
+          if (c == ob / kWarp) nn[c] = b0;
+          if (c == ob / kWarp + 1) nn[c] = b1;
+        }
+      } else {
+        if (v0) {
+          const unsigned long long k = ordered_key(a0);
+          if (!have || k > best_key) { best_key = k; best_idx = o0; have = true; }
+        }
+        if (v1) {
+          const unsigned long long k = ordered_key(a1);
+          if (!have || k > best_key) { best_key = k; best_idx = o1; have = true; }
+        }
+      }
+    }
+    __syncwarp();
+    cur = dst;
+#pragma unroll
+    for (int c = 0; c < kMlpMaskWords; ++c) nz[c] = nn[c];
+  }
+  const unsigned long long gmax = warp_max_u64(have ? best_key : 0ull);
+  const int cand = (have && best_key == gmax) ? best_idx : 0x7fffffff;
+  return warp_min(cand);
+}
+
+// Element k of the reference flat vector -> its slot in the transposed layout.
+__device__ __forceinline__ void mlp_transpose_elem(const double* __restrict__ params, int layers,
+                                                   const int* dims, const int* woff,
+                                                   const int* boff, double* out, size_t k) {
+  size_t src = 0;
+  for (int layer = 0; layer < layers; ++layer) {
+    const int ni = dims[layer], no = dims[layer + 1];
+    const size_t nw = (size_t)ni * no;
+    if (k < src + nw) {
+      const size_t e = k - src;
+      const int o = (int)(e / ni), i = (int)(e - (size_t)o * ni);
+      out[woff[layer] + (size_t)i * no + o] = params[k];
+      return;
+    }
+    if (k < src + nw + no) {
+      out[boff[layer] + (k - src - nw)] = params[k];
+      return;
+    }
+    src += nw + no;
+  }
+}
+
+struct MlpTransposeArgs {
+  const double* params;
+  int layers;
+  int dims[RS_MAX_LAYERS + 1];
+  int woff[RS_MAX_LAYERS], boff[RS_MAX_LAYERS];
+  double* out;
+  size_t count;
+};
+
+// Global-memory transposed copy for Q-networks too large to stage in smem.
+template <int Unused = 0>
+__global__ void mlp_transpose_kernel(const __grid_constant__ MlpTransposeArgs A) {
+  const size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < A.count) mlp_transpose_elem(A.params, A.layers, A.dims, A.woff, A.boff, A.out, k);
 }
 
 // Cooperative (whole CTA) copy of the reference flat parameter vector

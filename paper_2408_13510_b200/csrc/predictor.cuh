@@ -62,7 +62,7 @@ predict_kernel(const __grid_constant__ PredParams P) {
     }
     // predict_simulated (predictor.hpp:98-110) over one mt19937_64 stream
     const int nb = P.n_pred_edges;
-    mt_seed_warp(st, P.seeds[r]);
+    mt_seed_warp(st, P.seeds[r], l);
     int pos = 312;  // next unread output in `ob`
     for (int base = 0; base < n; base += kWarp) {
       const int i = base + l;
@@ -80,7 +80,7 @@ predict_kernel(const __grid_constant__ PredParams P) {
         int pj = 0;
         if (nb > 1) {
           if (pos == 312) {
-            mt_twist_warp(st);
+            mt_twist_warp(st, l);
             for (int k = l; k < 312; k += kWarp) ob[k] = mt_temper(st[k]);
             __syncwarp();
             pos = 0;
@@ -94,7 +94,7 @@ predict_kernel(const __grid_constant__ PredParams P) {
             pj = nb - 2;
           } else {
             if (pos == 312) {
-              mt_twist_warp(st);
+              mt_twist_warp(st, l);
               for (int k = l; k < 312; k += kWarp) ob[k] = mt_temper(st[k]);
               __syncwarp();
               pos = 0;

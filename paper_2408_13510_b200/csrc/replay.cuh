@@ -442,7 +442,7 @@ __device__ inline int inst_step(const KParams& P, const Grp& G, long long off, i
         if (k * kWarp < n) {
           const bool v = k * kWarp + l < n;
           const int x = v ? e_pm[k] : 0;
-          const int incl = warp_incl_scan(x) + carry;
+          const int incl = warp_incl_scan(x, l) + carry;
           const int excl = incl - x;
           const int take = min(budget, incl) - min(budget, excl);
           emits[k] = v && x == 0;  // co-decoders

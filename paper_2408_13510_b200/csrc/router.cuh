@@ -36,7 +36,7 @@ __device__ __forceinline__ bool can_accept(const KParams& P, const Feat& f, int 
 
 // capacity_fraction (instance.hpp:138-142)
 __device__ __forceinline__ double capacity_of(const KParams& P, int kv) {
-  double v = __dsub_rn(1.0, __ddiv_rn((double)kv, (double)P.kv_cap));
+  double v = __dsub_rn(1.0, div_exact((double)kv, (double)P.kv_cap, P.inv_kv, P.kv_pow2));
   return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
 }
 
@@ -51,10 +51,10 @@ __device__ __forceinline__ void store_inst(const Grp& G, int i, const InstHot& h
 }
 
 // Head-window: request data of the range head (prompt, true decode, bucket).
-__device__ __forceinline__ void head_window(const KParams& P, Replay& R, int q) {
+__device__ __forceinline__ void head_window(const KParams& P, Replay& R, int q, int l) {
   if (q >= R.h_base && q < R.h_base + kWarp) return;
   R.h_base = q & ~(kWarp - 1);
-  const int j = R.h_base + lane_id();
+  const int j = R.h_base + l;
   if (j < R.n) {
     R.h_prompt = P.prompt[R.off + j];
     R.h_true = P.decode[R.off + j];
@@ -62,9 +62,10 @@ __device__ __forceinline__ void head_window(const KParams& P, Replay& R, int q) 
   }
 }
 
-__device__ __forceinline__ Rec load_req(const KParams& P, long long off, int req, int* bucket) {
+__device__ __forceinline__ Rec load_req(const KParams& P, long long off, int req, int* bucket,
+                                       int l) {
   int v[3] = {0, 0, 0};
-  if (lane_id() == 0) {
+  if (l == 0) {
     v[0] = P.prompt[off + req];
     v[1] = P.decode[off + req];
     v[2] = P.bucket[off + req];
@@ -80,9 +81,10 @@ __device__ __forceinline__ Rec load_req(const KParams& P, long long off, int req
 }
 
 template <int POL>
-__device__ __forceinline__ Rec head_rec(const KParams& P, int* front, Replay& R, int* bucket) {
-  if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) return load_req(P, R.off, front[0], bucket);
-  head_window(P, R, R.qhead);
+__device__ __forceinline__ Rec head_rec(const KParams& P, int* front, Replay& R, int* bucket,
+                                       int l) {
+  if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) return load_req(P, R.off, front[0], bucket, l);
+  head_window(P, R, R.qhead, l);
   const int s = R.qhead - R.h_base;
   Rec r;
   r.req = R.qhead;
@@ -94,21 +96,21 @@ __device__ __forceinline__ Rec head_rec(const KParams& P, int* front, Replay& R,
   return r;
 }
 
-__device__ __forceinline__ void load_arrival_window(const KParams& P, Replay& R) {
-  const int j = R.a_base + lane_id();
+__device__ __forceinline__ void load_arrival_window(const KParams& P, Replay& R, int l) {
+  const int j = R.a_base + l;
   R.a_val = j < R.n ? P.arrival[R.off + j] : __longlong_as_double(0x7ff0000000000000ll);
 }
 
 // ClusterSim::inject_arrivals (env.hpp:357-375): predictions were resolved
 // by the predictor pre-pass, so injection is a cursor advance.
-__device__ __forceinline__ void inject(const KParams& P, Replay& R) {
+__device__ __forceinline__ void inject(const KParams& P, Replay& R, int l) {
   for (;;) {
-    const int j = R.a_base + lane_id();
+    const int j = R.a_base + l;
     const bool ok = j >= R.cursor && j < R.n && R.a_val <= R.clock;
     R.cursor += __popc(__ballot_sync(kFull, ok));
     if (R.cursor == R.a_base + kWarp && R.cursor < R.n) {
       R.a_base += kWarp;
-      load_arrival_window(P, R);
+      load_arrival_window(P, R, l);
       continue;
     }
     break;
@@ -122,10 +124,10 @@ __device__ __forceinline__ int queue_len(const Replay& R) {
 }
 
 // Skip range entries that min_min moved to the front list.
-__device__ __forceinline__ void mm_skip_removed(const KParams& P, Replay& R) {
+__device__ __forceinline__ void mm_skip_removed(const KParams& P, Replay& R, int l) {
   while (R.qhead < R.cursor && R.n_removed > 0) {
     int rem = 0;
-    if (lane_id() == 0) rem = P.mm_removed[R.off + R.qhead];
+    if (l == 0) rem = P.mm_removed[R.off + R.qhead];
     rem = __shfl_sync(kFull, rem, 0);
     if (!rem) break;
     R.qhead++;
@@ -136,8 +138,7 @@ __device__ __forceinline__ void mm_skip_removed(const KParams& P, Replay& R) {
 // MinMinPolicy::pick_queue_index (policies.hpp:179-191) + move_to_front
 // (env.hpp:234-243).  Queue order = front list, then the range in index
 // order minus removed entries.  Returns false on front-list overflow.
-__device__ inline bool minmin_pick(const KParams& P, int* front, Replay& R) {
-  const int l = lane_id();
+__device__ inline bool minmin_pick(const KParams& P, int* front, Replay& R, int l) {
   unsigned long long fk = ~0ull;
   int fpos = 0x7fffffff;
   if (R.nfront > 0) {
@@ -192,17 +193,18 @@ __device__ inline bool minmin_pick(const KParams& P, int* front, Replay& R) {
   __syncwarp();
   R.nfront++;
   R.n_removed++;
-  mm_skip_removed(P, R);
+  mm_skip_removed(P, R, l);
   return true;
 }
 
 // ε-greedy stream (DqnAgent::act, dqn.hpp:92-99) in shared memory.
-__device__ __forceinline__ unsigned long long rng_draw(unsigned long long* rngbuf, Replay& R) {
+__device__ __forceinline__ unsigned long long rng_draw(unsigned long long* rngbuf, Replay& R,
+                                                       int l) {
   unsigned long long* st = rngbuf;
   unsigned long long* ob = rngbuf + 312;
   if (R.rng_pos == 312) {
-    mt_twist_warp(st);
-    for (int k = lane_id(); k < 312; k += kWarp) ob[k] = mt_temper(st[k]);
+    mt_twist_warp(st, l);
+    for (int k = l; k < 312; k += kWarp) ob[k] = mt_temper(st[k]);
     __syncwarp();
     R.rng_pos = 0;
   }
@@ -282,16 +284,16 @@ __device__ inline int decide(const KParams& P, const Grp& G, const MlpView& M, R
     __syncwarp();
     const int na = P.rl_dims[P.rl_layers];
     if (P.rl_eps > 0.0) {
-      const double u = u01(rng_draw(G.rng, R));
+      const double u = u01(rng_draw(G.rng, R, l));
       if (u < P.rl_eps) {
-        const double v = __dmul_rn(u01(rng_draw(G.rng, R)), (double)na);
+        const double v = __dmul_rn(u01(rng_draw(G.rng, R, l)), (double)na);
         const unsigned long long k = (unsigned long long)v;  // static_cast<uint64_t>
         return (int)(k < (unsigned long long)na ? k : (unsigned long long)na - 1);
       }
     }
     double* h0 = x + M.dims[0];
     double* h1 = h0 + P.rl_maxw;
-    return mlp_forward_warp(M, x, h0, h1, nullptr);
+    return mlp_forward_warp(M, x, h0, h1, nullptr, l);
   } else {
     // argmin policies: decode_balancer / jsq / min_min / workload_aware
     if (!has_head) return m;
@@ -340,8 +342,7 @@ __device__ inline int decide(const KParams& P, const Grp& G, const MlpView& M, R
 
 // Per-replay statistics (compute_metrics, metrics.hpp:84-162): fp64 sums are
 // sequential in pool-index order, bit-identical to the reference.
-__device__ inline void write_replay_stats(const KParams& P, const Replay& R, int r) {
-  const int l = lane_id();
+__device__ inline void write_replay_stats(const KParams& P, const Replay& R, int r, int l) {
   double se = 0.0, st = 0.0, sb = 0.0, sw = 0.0;
   long long tbtc = 0, pre = 0, tok = 0;
   double fa = __longlong_as_double(0x7fefffffffffffffll), lc = 0.0;
@@ -488,25 +489,25 @@ __device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int
   R.h_base = -2 * kWarp;
   R.h_prompt = R.h_true = R.h_bucket = 0;
   if (POL == RS_POLICY_RL && P.rl_eps > 0.0)
-    mt_seed_warp(G.rng, P.policy_seed ? P.policy_seed[r] : 0ull);
+    mt_seed_warp(G.rng, P.policy_seed ? P.policy_seed[r] : 0ull, l);
   __syncwarp();
-  load_arrival_window(P, R);
+  load_arrival_window(P, R, l);
   if (bad) {
     R.status = RS_REPLAY_INVALID_TRACE;
   } else {
-    inject(P, R);  // ctor (env.hpp:193)
+    inject(P, R, l);  // ctor (env.hpp:193)
   }
 
   // ---------------------------------------------------------- tick loop
   while (R.status == RS_REPLAY_FINISHED && R.completed != R.n && R.tick < P.max_ticks) {
     if (POL == RS_POLICY_MIN_MIN && queue_len<POL>(R) > 0) {
-      if (!minmin_pick(P, G.front, R)) { R.status = RS_REPLAY_CAPACITY; break; }
+      if (!minmin_pick(P, G.front, R, l)) { R.status = RS_REPLAY_CAPACITY; break; }
     }
     const bool has_head = queue_len<POL>(R) > 0;
     Rec hr;
     int hb = 0;
     if (has_head) {
-      hr = head_rec<POL>(P, G.front, R, &hb);
+      hr = head_rec<POL>(P, G.front, R, &hb, l);
     } else {
       hr.req = hr.prompt = hr.dhat = hr.tru = hr.emit = 0;
     }
@@ -525,7 +526,7 @@ __device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int
           R.nfront--;
         } else {
           R.qhead++;
-          if (POL == RS_POLICY_MIN_MIN) mm_skip_removed(P, R);
+          if (POL == RS_POLICY_MIN_MIN) mm_skip_removed(P, R, l);
         }
         if (l == 0) {
           P.o_routed[R.off + hr.req] = R.clock;
@@ -576,14 +577,14 @@ __device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int
     if (R.status != RS_REPLAY_FINISHED) break;
     R.completed += comps;
     R.clock = t1;
-    inject(P, R);
+    inject(P, R, l);
     R.tick++;
     R.sum_q += queue_len<POL>(R);
     R.sum_w += R.total_wait;
   }
   if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
 
-  write_replay_stats(P, R, r);
+  write_replay_stats(P, R, r, l);
 }
 
 template <int POL>
@@ -598,9 +599,13 @@ __global__ void __launch_bounds__(256) replay_kernel(const __grid_constant__ KPa
   M.w = reinterpret_cast<const double*>(smem);
   int groups_off = 0;
   if (POL == RS_POLICY_RL) {
-    mlp_stage_weights(P.rl_w, P.rl_layers, P.rl_dims, P.rl_woff, P.rl_boff,
-                      reinterpret_cast<double*>(smem));
-    groups_off = P.smem_weights_bytes;
+    if (P.rl_wt_global) {  // too big for shared memory: transposed copy in L2
+      M.w = P.rl_wt_global;
+    } else {
+      mlp_stage_weights(P.rl_w, P.rl_layers, P.rl_dims, P.rl_woff, P.rl_boff,
+                        reinterpret_cast<double*>(smem));
+      groups_off = P.smem_weights_bytes;
+    }
   }
   char* gbase = smem + groups_off + (size_t)w * P.smem_group_bytes;
   const Grp G = make_grp(P, gbase);

@@ -37,8 +37,7 @@ _ref = None
 def ora_lib() -> C.CDLL:
     global _ora
     if _ora is None:
-        if not ORA_PATH.exists():
-            _make("oracle")
+        _make("oracle")  # no-op when up to date; rebuilds after header changes
         lib = C.CDLL(str(ORA_PATH))
         P = C.POINTER
         lib.ora_run_replay.argtypes = [P(abi.BatchCfg), C.c_int64] + [C.c_void_p] * 5 + [

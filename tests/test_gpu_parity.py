@@ -104,8 +104,12 @@ def test_batched_replays_match_oracle(gpu, pol):
         assert O.compare(got[r], want) == [], f"replay {r}"
 
 
-@pytest.mark.parametrize("m,eps", [(4, 0.0), (8, 0.0), (4, 0.3), (2, 0.0)])
-def test_rl_router_matches_oracle(gpu, m, eps):
+@pytest.mark.parametrize("m,eps,glob", [(4, 0.0, 0), (8, 0.0, 0), (4, 0.3, 0), (2, 0.0, 0),
+                                        (8, 0.0, 1), (64, 0.0, 0)])
+def test_rl_router_matches_oracle(gpu, m, eps, glob, monkeypatch):
+    # glob=1 forces the global-memory (L2) weights path; m=64 needs it anyway
+    if glob:
+        monkeypatch.setenv("RS_RL_GLOBAL", "1")
     sd = abi.state_dimension(m)
     rng = np.random.default_rng(m)
     dims = [sd, 64, 64, m + 1]

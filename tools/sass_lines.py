@@ -67,7 +67,7 @@ def main():
         tot += v
     ts = sum(stall.values()) or 1
     print(f"total {metric}: {tot:.4g}")
-    for (f, l), v in sorted(agg.items(), key=lambda kv: -stall[kv[0]])[:45]:
+    for (f, l), v in sorted(agg.items(), key=lambda kv: -stall[kv[0]])[:int(__import__("os").environ.get("TOPN","45"))]:
         print(f"{f}:{l:<5d} instr {100 * v / tot:5.1f}%   stall-samples {100 * stall[(f, l)] / ts:5.1f}%")
 
 
