@@ -1,0 +1,73 @@
+#!/usr/bin/env python
+"""Summarise an ncu report (one kernel launch) into JSON for profiles/.
+
+    python tools/ncu_summary.py <report.ncu-rep> <out.json> [--alg-bytes B] [--note TEXT]
+
+Keeps: duration, DRAM read/write bytes (the bench's roofline `traffic`),
+instructions, issue activity, occupancy, warp-stall breakdown (cycles per
+issued instruction) and launch shape.  Units are normalised (bytes, ns).
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+         "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9,
+         "ns": 1, "us": 1e3, "ms": 1e6, "s": 1e9}
+
+
+def main():
+    rep, out = sys.argv[1], sys.argv[2]
+    alg = None
+    note = ""
+    if "--alg-bytes" in sys.argv:
+        alg = float(sys.argv[sys.argv.index("--alg-bytes") + 1])
+    if "--note" in sys.argv:
+        note = sys.argv[sys.argv.index("--note") + 1]
+    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    d, u = dict(zip(hdr, vals)), dict(zip(hdr, units))
+
+    def num(k):
+        try:
+            return float(d[k].replace(",", "")) * SCALE.get(u.get(k, ""), 1)
+        except (KeyError, ValueError):
+            return None
+
+    s = {
+        "kernel": d.get("Kernel Name"),
+        "report": rep.split("/")[-1],
+        "duration_ns": num("gpu__time_duration.sum"),
+        "dram_read_bytes": num("dram__bytes_read.sum"),
+        "dram_write_bytes": num("dram__bytes_write.sum"),
+        "inst_executed": num("smsp__inst_executed.sum"),
+        "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+        "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
+        "registers_per_thread": num("launch__registers_per_thread"),
+        "block_size": num("launch__block_size"),
+        "grid_size": num("launch__grid_size"),
+        "stall_cycles_per_issue": {},
+        "note": note,
+    }
+    if s["dram_read_bytes"] is not None and s["dram_write_bytes"] is not None:
+        s["dram_bytes_per_launch"] = s["dram_read_bytes"] + s["dram_write_bytes"]
+        if s["duration_ns"]:
+            s["dram_gbs"] = s["dram_bytes_per_launch"] / s["duration_ns"]
+    if alg:
+        s["algorithmic_bytes_per_launch"] = alg
+    for k in hdr:
+        if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
+            v = num(k)
+            if v and v > 0.01:
+                s["stall_cycles_per_issue"][k[len("smsp__average_warps_issue_stalled_"):-len(
+                    "_per_issue_active.ratio")]] = round(v, 3)
+    json.dump(s, open(out, "w"), indent=1)
+    print(json.dumps(s, indent=1))
+
+
+if __name__ == "__main__":
+    main()
