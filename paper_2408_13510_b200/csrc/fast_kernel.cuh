@@ -182,6 +182,15 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
     return mlp_forward_warp(M, x, h0, h1, nullptr, l);
   } else {  // argmin policies
     if (!has_head) return m;
+    if (POL == RS_POLICY_DECODE_BALANCER || POL == RS_POLICY_WORKLOAD_AWARE) {
+      // a saturated fleet defers most ticks: skip the scores when no
+      // instance can take the head (the reference's result is `defer`)
+      bool any_ok = false;
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        any_ok |= (g * kWarp + l < m) && can_accept(P, feat_of(S[g]), need);
+      if (!__any_sync(kFull, any_ok)) return m;
+    }
     unsigned long long bk = ~0ull;
     int bi = -1;
 #pragma unroll
@@ -281,9 +290,18 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
                  P.policy_seed ? P.policy_seed[r] : 0ull, l);
   __syncwarp();
   load_arrival_window(P, R, l);
+  // arrival time of the next request to inject (+inf when none is left)
+  auto next_arrival = [&]() {
+    const int k = R.cursor - R.a_base;
+    const double a = __shfl_sync(kFull, R.a_val, k & (kWarp - 1));
+    R.next_arr = R.cursor < R.n ? a : __longlong_as_double(0x7ff0000000000000ll);
+  };
+  R.hr_q = -1;
+  R.hr_prompt = R.hr_true = R.hr_bucket = 0;
   if (bad) R.status = RS_REPLAY_INVALID_TRACE;
   else if (too_big) R.status = RS_REPLAY_CAPACITY;
   else inject(P, R, l);
+  next_arrival();
 
   while (R.status == RS_REPLAY_FINISHED && R.completed != R.n && R.tick < P.max_ticks) {
     if (POL == RS_POLICY_MIN_MIN && queue_len<POL>(R) > 0) {
@@ -292,8 +310,24 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
     const bool has_head = queue_len<POL>(R) > 0;
     Rec hr;
     int hb = 0;
-    if (has_head) hr = head_rec<POL>(P, front, R, &hb, l);
-    else hr.req = hr.prompt = hr.dhat = hr.tru = hr.emit = 0;
+    if (has_head) {
+      if (POL != RS_POLICY_MIN_MIN && R.hr_q == R.qhead) {  // same head as last tick
+        hr.req = R.qhead;
+        hr.prompt = R.hr_prompt;
+        hr.tru = R.hr_true;
+        hb = R.hr_bucket;
+        hr.dhat = P.ub[hb];
+        hr.emit = 0;
+      } else {
+        hr = head_rec<POL>(P, front, R, &hb, l);
+        R.hr_q = hr.req;
+        R.hr_prompt = hr.prompt;
+        R.hr_true = hr.tru;
+        R.hr_bucket = hb;
+      }
+    } else {
+      hr.req = hr.prompt = hr.dhat = hr.tru = hr.emit = 0;
+    }
     const int action = decide_fast<POL, G>(P, gw, M, R, S, has_head, hr, hb, gbase, l);
     R.hash = hash_action(R.hash, action);
     if (action < 0 || action > m) { R.status = RS_REPLAY_BAD_ACTION; break; }
@@ -317,32 +351,41 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
           P.o_instance[off + hr.req] = action;
         }
         R.routed++;
+        R.total_wait++;  // the enqueue (uniform; admissions are counted per lane)
 #pragma unroll
         for (int g = 0; g < G; ++g)
           if (g * kWarp + l == action) {
             lane_enqueue(P, gw, off, action, S[g], hr, R.clock);
-            wdelta++;
           }
       }
     }
 
     // ---- run_until(t1) for every instance (env.hpp:277-287) -----------
-    for (;;) {
-      bool act[G];
-      unsigned any = 0;
+    // One warp collective per iteration: an OR-reduction of (event | again).
+    bool act[G];
+    bool again = false;
 #pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const int i = g * kWarp + l;
-        act[g] = false;
-        if (i < m && S[g].clock < t1) {
-          if (S[g].n > 0 || S[g].w_cnt > 0) act[g] = true;
-          else S[g].clock = t1;  // idle instance skips ahead (instance.hpp:309)
-        }
-        any |= act[g] ? (1u << g) : 0u;
+    for (int g = 0; g < G; ++g) {
+      const int i = g * kWarp + l;
+      act[g] = false;
+      if (i < m && S[g].clock < t1) {
+        if (S[g].n > 0 || S[g].w_cnt > 0) act[g] = true;
+        else S[g].clock = t1;  // idle instance skips ahead (instance.hpp:309)
       }
-      const unsigned am = __ballot_sync(kFull, any != 0);
-      if (!am) break;
+      again |= act[g];
+    }
+    unsigned fl = __any_sync(kFull, again) ? 2u : 0u;
+    while (fl & 2u) {
       if (seq) {  // only the lowest-index instance that still has work
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int i = g * kWarp + l;
+          act[g] = false;
+          if (i < m && S[g].clock < t1) {
+            if (S[g].n > 0 || S[g].w_cnt > 0) act[g] = true;
+            else S[g].clock = t1;
+          }
+        }
         int g0 = G;
 #pragma unroll
         for (int g = G - 1; g >= 0; --g)
@@ -358,6 +401,11 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
         if (!act[g]) continue;
         Inst& I = S[g];
         const int i = g * kWarp + l;
+        if (I.n == 0 && I.w_cnt == 0) {  // emptied by last iteration's events
+          I.clock = t1;
+          act[g] = false;
+          continue;
+        }
         if (I.w_cnt > 0 && I.n < P.max_batch) {
           const int w0 = I.w_cnt + I.o_cnt;
           lane_admit(P, gw, off, i, I);
@@ -402,8 +450,19 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
           }
         }
       }
-      unsigned evm = __ballot_sync(kFull, ev);
-      if (!evm) continue;
+      // a stepped instance steps again while its clock is behind t1 (it has
+      // work: only events can empty it, and the next iteration checks that)
+      again = false;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        act[g] = act[g] && S[g].clock < t1;
+        // sequential mode keeps going while ANY instance still has a step
+        again |= seq ? (g * kWarp + l < m && S[g].clock < t1 &&
+                        (S[g].n > 0 || S[g].w_cnt > 0))
+                     : act[g];
+      }
+      fl = (__any_sync(kFull, again) ? 2u : 0u) | (__any_sync(kFull, ev) ? 1u : 0u);
+      if (!(fl & 1u)) continue;
       // ---- events (whole warp): errors, completion scans, preemption ----
       {
         int err = kBig;
@@ -443,13 +502,21 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
     for (int g = 0; g < G; ++g) {
       comps += S[g].comps;
       S[g].comps = 0;
+      // instances emptied by this tick's last events skip ahead (instance.hpp:309)
+      if (S[g].clock < t1 && S[g].n == 0 && S[g].w_cnt == 0) S[g].clock = t1;
     }
     // one reduction: completions (low 16 bits) + biased waiting deltas
-    const unsigned packed = warp_sum((int)((unsigned)comps | ((unsigned)(wdelta + 1024) << 16)));
-    R.completed += (int)(packed & 0xffffu);
-    R.total_wait += (int)(packed >> 16) - kWarp * 1024;
+    if (__any_sync(kFull, (comps | wdelta) != 0)) {
+      const unsigned packed =
+          warp_sum((int)((unsigned)comps | ((unsigned)(wdelta + 1024) << 16)));
+      R.completed += (int)(packed & 0xffffu);
+      R.total_wait += (int)(packed >> 16) - kWarp * 1024;
+    }
     R.clock = t1;
-    inject(P, R, l);
+    if (R.clock >= R.next_arr) {  // inject_arrivals (env.hpp:357-375) only when due
+      inject(P, R, l);
+      next_arrival();
+    }
     R.tick++;
     R.sum_q += queue_len<POL>(R);
     R.sum_w += R.total_wait;

@@ -57,6 +57,10 @@ struct Replay {  // per-replay registers (uniform across the warp)
   double a_val;    // arrival[a_base + lane]
   int h_base;      // head window base
   int h_prompt, h_true, h_bucket;
+  // fast kernel: arrival time of request `cursor` (+inf when all arrived)
+  // and the cached head record (valid while qhead == hr_q)
+  double next_arr;
+  int hr_q, hr_prompt, hr_true, hr_bucket;
 };
 
 __device__ __forceinline__ Grp make_grp(const KParams& P, char* base) {
