@@ -41,6 +41,7 @@ METRIC = "routing decisions/sec over batched trace replays (whole box) at 1/2/4/
 UNIT = "decisions/s"
 REPLAY_BYTES_PER_REQUEST = 8 + 4 + 4 + 1 + (4 + 8 + 8 + 8 + 4)  # in: arrival, prompt, decode, bucket; out
 REPLAY_BYTES_PER_REPLAY = 8 + 256  # offsets + stats record
+PREWARM_S = 2.0
 
 CONFIGS = {
     # name: (requests, replays per GPU, instances, rate, policy, weights, description)
@@ -273,6 +274,13 @@ def main():
         if world > 1:  # final gather of the per-replay statistics (NCCL)
             dist.all_gather_into_tensor(gathered, d_st)
 
+    # Pre-warm: a fresh box's first seconds of work run ~35% slower (clock /
+    # power ramp; measured), so repeat untimed full steps for >= PREWARM_S
+    # before the W warm-up steps.  Reported in config.prewarm_s.
+    t_pw = time.perf_counter()
+    while time.perf_counter() - t_pw < PREWARM_S:
+        step()
+        torch.cuda.synchronize(dev)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
@@ -373,7 +381,8 @@ def main():
                    "predictor": "simulated, Table-1 accuracy",
                    "l2": f"inputs {(8 + 4 + 4 + 1) * N / 1e6:.0f} MB per GPU > 126 MB L2 "
                          "(no flush needed)",
-                   "parallelism": f"replay shards x{world} (weak)"},
+                   "parallelism": f"replay shards x{world} (weak)",
+                   "prewarm_s": PREWARM_S},
         "decisions_per_step": ticks_total, "unfinished_replays": unfinished,
         "gpu_launches": 2 * args.steps * world,
         "kernel_ms": {"predict_buckets": pred_s * 1e3, "replay": replay_s * 1e3},

@@ -99,7 +99,10 @@ Layout make_layout(const rs_batch_cfg& c, int wcap, bool fast) {
   if (rl) {
     for (int l = 1; l < c.rl_num_layers; ++l) L.maxw = std::max(L.maxw, c.rl_dims[l]);
     L.maxw = std::max(L.maxw, 1);
-    off = align_up(off + (size_t)(c.rl_dims[0] + 2 * L.maxw) * sizeof(double), 16);
+    // x, h0, h1, then the nonzero-input list (values, then int row offsets)
+    const size_t lmax = (size_t)std::max(c.rl_dims[0], L.maxw);
+    off = align_up(off + (size_t)(c.rl_dims[0] + 2 * L.maxw + lmax) * sizeof(double) +
+                       lmax * sizeof(int), 16);
   }
   L.off_rng = (int)off;
   if (rl && c.rl_epsilon > 0.0) off = align_up(off + 624 * sizeof(unsigned long long), 16);
@@ -606,6 +609,22 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
   if (best_wpb == 0)
     return fail(RS_ERR_UNSUPPORTED, "per-replay shared-memory state exceeds one SM (" +
                                         std::to_string(L.weights_bytes + L.group_bytes) + " B)");
+  // When every replay fits in one wave, the kernel time is the slowest
+  // warp's: spread the replays evenly, ceil(R / #SMs) warps per SM (one
+  // block per SM when that is <= 8 warps), instead of packing some SMs.
+  {
+    int sms = 0;
+    RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int need = (tr->num_replays + sms - 1) / std::max(1, sms);
+    if (!wpb_env && need <= best_warps && need <= 8) {
+      for (int wpb = need; wpb >= 1; --wpb) {
+        if (L.weights_bytes + wpb * L.group_bytes <= smem_optin) {
+          best_wpb = wpb;
+          break;
+        }
+      }
+    }
+  }
   const int block_smem = L.weights_bytes + best_wpb * L.group_bytes;
   RS_CUDA(cudaMemsetAsync(kp.work_counter, 0, sizeof(int), st));
   KernelFn kern = kernel_for(cfg->policy, fast, groups);

@@ -136,12 +136,24 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
         int cge[RS_MAX_BUCKETS + 1];
 #pragma unroll
         for (int b = 0; b < RS_MAX_BUCKETS; ++b) cge[b] = 0;
-        for (int j = 0; j < S[g].n; ++j) {
-          int d = RD(P, gw, i, j) - (S[g].D + RK(P, gw, i, j));
-          d = d > 0 ? d : 0;
+        if (nsb == 3) {  // BucketScheme::state_default {0, 256, 2048}
+          const int e1 = P.state_edges[1], e2 = P.state_edges[2];
+          int c1 = 0, c2 = 0;
+          for (int j = 0; j < S[g].n; ++j) {
+            const int d = RD(P, gw, i, j) - (S[g].D + RK(P, gw, i, j));
+            c1 += d >= e1;
+            c2 += d >= e2;
+          }
+          cge[1] = c1;
+          cge[2] = c2;
+        } else {
+          for (int j = 0; j < S[g].n; ++j) {
+            int d = RD(P, gw, i, j) - (S[g].D + RK(P, gw, i, j));
+            d = d > 0 ? d : 0;
 #pragma unroll
-          for (int b = 1; b < RS_MAX_BUCKETS; ++b)
-            if (b < nsb) cge[b] += d >= P.state_edges[b];
+            for (int b = 1; b < RS_MAX_BUCKETS; ++b)
+              if (b < nsb) cge[b] += d >= P.state_edges[b];
+          }
         }
 #pragma unroll
         for (int b = 0; b < RS_MAX_BUCKETS; ++b) {
@@ -174,8 +186,10 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
     }
     if (!P.rl_wt_global) {  // staged weights: LDS-only forward over nonzero inputs
       const int xd = (gw >> 1) + (P.off_rlx >> 3);
-      return mlp_forward_smem(P.rl_dims, P.rl_woff, P.rl_boff, P.rl_layers, xd,
-                              xd + P.rl_dims[0], xd + P.rl_dims[0] + P.rl_maxw, l);
+      const int h0d = xd + P.rl_dims[0], h1d = h0d + P.rl_maxw, lvd = h1d + P.rl_maxw;
+      const int lmax = P.rl_dims[0] > P.rl_maxw ? P.rl_dims[0] : P.rl_maxw;
+      return mlp_forward_list(P.rl_dims, P.rl_woff, P.rl_boff, P.rl_layers, xd, h0d, h1d, lvd,
+                              (lvd + lmax) * 2, l);
     }
     double* h0 = x + M.dims[0];
     double* h1 = h0 + P.rl_maxw;

@@ -171,6 +171,77 @@ __device__ inline int mlp_forward_smem(const int* dims, const int* woff, const i
   return warp_min(cand);
 }
 
+// Forward with weights staged in shared memory (double index 0), x / h0 / h1
+// at double indices xd / h0d / h1d, and a per-warp list of the current
+// layer's nonzero inputs (value at lvd + k, W^T row offset at int index
+// lid + k) compacted in ascending index order.  The accumulation is then a
+// counted loop (unrolled, loads prefetched) over the nonzero terms only:
+// each output still adds w*x for i = 0..ni-1 in order, zero terms omitted
+// exactly as in mlp_forward_warp.
+__device__ inline int mlp_forward_list(const int* dims, const int* woff, const int* boff,
+                                       int layers, int xd, int h0d, int h1d, int lvd, int lid,
+                                       int l) {
+  int* rs_smi = reinterpret_cast<int*>(rs_smd);
+  const unsigned lt = lanemask_lt();
+  int cur = xd;
+  unsigned long long best_key = 0;
+  int best_idx = 0x7fffffff;
+  bool have = false;
+  for (int layer = 0; layer < layers; ++layer) {
+    const int ni = dims[layer], no = dims[layer + 1];
+    const int wt = woff[layer], bs = boff[layer];
+    // compact the nonzero inputs of `cur`
+    int nnz = 0;
+    for (int c = 0; c < ni; c += kWarp) {
+      const int i = c + l;
+      const double v = i < ni ? rs_smd[cur + i] : 0.0;
+      const bool nz = v != 0.0;
+      const unsigned msk = __ballot_sync(kFull, nz);
+      if (nz) {
+        const int p = nnz + __popc(msk & lt);
+        rs_smd[lvd + p] = v;
+        rs_smi[lid + p] = wt + i * no;
+      }
+      nnz += __popc(msk);
+    }
+    __syncwarp();
+    const bool last = layer + 1 == layers;
+    const int dst = (layer & 1) ? h1d : h0d;
+    for (int ob = 0; ob < no; ob += 2 * kWarp) {
+      const int o0 = ob + l, o1 = ob + kWarp + l;
+      const bool v0 = o0 < no, v1 = o1 < no;
+      double a0 = v0 ? rs_smd[bs + o0] : 0.0;
+      double a1 = v1 ? rs_smd[bs + o1] : 0.0;
+      const int c0 = v0 ? o0 : 0, c1 = v1 ? o1 : 0;
+#pragma unroll 4
+      for (int k = 0; k < nnz; ++k) {
+        const double xv = rs_smd[lvd + k];
+        const int row = rs_smi[lid + k];
+        a0 = __dadd_rn(a0, __dmul_rn(rs_smd[row + c0], xv));
+        a1 = __dadd_rn(a1, __dmul_rn(rs_smd[row + c1], xv));
+      }
+      if (!last) {
+        if (v0) rs_smd[dst + o0] = a0 > 0.0 ? a0 : 0.0;
+        if (v1) rs_smd[dst + o1] = a1 > 0.0 ? a1 : 0.0;
+      } else {
+        if (v0) {
+          const unsigned long long k = ordered_key(a0);
+          if (!have || k > best_key) { best_key = k; best_idx = o0; have = true; }
+        }
+        if (v1) {
+          const unsigned long long k = ordered_key(a1);
+          if (!have || k > best_key) { best_key = k; best_idx = o1; have = true; }
+        }
+      }
+    }
+    __syncwarp();
+    cur = dst;
+  }
+  const unsigned long long gmax = warp_max_u64(have ? best_key : 0ull);
+  const int cand = (have && best_key == gmax) ? best_idx : 0x7fffffff;
+  return warp_min(cand);
+}
+
 // Element k of the reference flat vector -> its slot in the transposed layout.
 __device__ __forceinline__ void mlp_transpose_elem(const double* __restrict__ params, int layers,
                                                    const int* dims, const int* woff,
