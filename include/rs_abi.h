@@ -163,6 +163,11 @@ typedef struct rs_batch_cfg {
 } rs_batch_cfg;
 
 #define RS_FLAG_NONE 0u
+/* rs_replay_batch draws the decode-length predictions itself, at arrival
+ * injection as the reference does (env.hpp:357-375), writing them to
+ * out->predicted_bucket; rs_predict_buckets is then not needed.  Needs
+ * trace->predictor_seed (simulated) or trace->given_bucket (given). */
+#define RS_FLAG_PREDICT_INLINE 1u
 
 /* Struct-of-arrays trace batch, CSR over replays.  Request i of replay r is
  * element offsets[r] + i.  Field meaning follows Request (request.hpp:42-69). */

@@ -47,6 +47,7 @@ POLICIES = {
 POLICY_NAMES = {v: k for k, v in POLICIES.items()}
 BATCHING = {"fcfs": 0, "bin_packing": 1, "least_work_left": 2}
 PRED_SIMULATED, PRED_EMPIRICAL, PRED_GIVEN = 0, 1, 2
+RS_FLAG_PREDICT_INLINE = 1  # rs_replay_batch draws predictions at injection
 
 # rs_replay_status
 REPLAY_FINISHED = 0

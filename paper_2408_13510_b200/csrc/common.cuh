@@ -120,6 +120,11 @@ struct KParams {
   double inv_eps, inv_kv, inv_mb;
   int eps_pow2, kv_pow2, mb_pow2;
   int ub_max;  // largest upper_bound_tokens (32-bit aggregate guard)
+  // fused predictor (fast kernel): predictions drawn at arrival injection
+  int predict_inline;
+  int off_pred;                    // mt19937_64 state + 312 outputs (bytes)
+  const uint64_t* predictor_seed;
+  const uint8_t* given_bucket;
 };
 
 // x / c, correctly rounded; a multiply when c is a power of two.

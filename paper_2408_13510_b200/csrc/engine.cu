@@ -19,6 +19,7 @@
 #include "predictor.cuh"
 #include "router.cuh"
 #include "fast_kernel.cuh"
+#include "stats.cuh"
 
 namespace {
 
@@ -65,7 +66,7 @@ rs_status require_device() {
 // Smem layout of one replay group (one warp) for this config.
 struct Layout {
   int rcap, wcap;
-  int off_run, off_wait, off_dbc, off_rlx, off_rng, off_front, group_bytes;
+  int off_run, off_wait, off_dbc, off_rlx, off_rng, off_front, off_pred, group_bytes;
   int weights_bytes;
   int woff[RS_MAX_LAYERS], boff[RS_MAX_LAYERS];
   int maxw;
@@ -108,6 +109,9 @@ Layout make_layout(const rs_batch_cfg& c, int wcap, bool fast) {
   if (rl && c.rl_epsilon > 0.0) off = align_up(off + 624 * sizeof(unsigned long long), 16);
   L.off_front = (int)off;
   if (c.policy == RS_POLICY_MIN_MIN) off = align_up(off + rs::kMaxFront * sizeof(int), 16);
+  L.off_pred = (int)off;  // fused predictor's mt19937_64 state + outputs
+  if (fast && (c.flags & RS_FLAG_PREDICT_INLINE) && c.predictor_mode == RS_PREDICTOR_SIMULATED)
+    off = align_up(off + 624 * sizeof(unsigned long long), 16);
   L.group_bytes = (int)align_up(off, 128);
   L.weights_bytes = 0;
   if (rl) {
@@ -528,6 +532,21 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
   kp.off_rlx = L.off_rlx;
   kp.off_rng = L.off_rng;
   kp.off_front = L.off_front;
+  kp.off_pred = L.off_pred;
+  kp.predictor_seed = tr->predictor_seed;
+  kp.given_bucket = tr->given_bucket;
+  if (cfg->flags & RS_FLAG_PREDICT_INLINE) {
+    if (cfg->predictor_mode == RS_PREDICTOR_SIMULATED && !tr->predictor_seed)
+      return fail(RS_ERR_INVALID_ARGUMENT, "simulated predictor needs trace->predictor_seed");
+    if (cfg->predictor_mode == RS_PREDICTOR_GIVEN && !tr->given_bucket)
+      return fail(RS_ERR_INVALID_ARGUMENT, "GIVEN predictor mode needs trace->given_bucket");
+    if (fast) {
+      kp.predict_inline = 1;  // drawn at injection inside the replay kernel
+    } else {
+      rs_status sp = rs_predict_buckets(cfg, tr, out->predicted_bucket, stream);
+      if (sp != RS_OK) return sp;
+    }
+  }
   {  // fast-kernel word offsets (fast.cuh RQ/RP/.../WE accessors)
     const int m = cfg->num_instances;
     kp.rstride = L.rcap | 1;
@@ -628,8 +647,26 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
   const int block_smem = L.weights_bytes + best_wpb * L.group_bytes;
   RS_CUDA(cudaMemsetAsync(kp.work_counter, 0, sizeof(int), st));
   KernelFn kern = kernel_for(cfg->policy, fast, groups);
-  if (kern) return launch_kernel(kern, kp, best_wpb, block_smem, tr->num_replays, st);
-  return fail(RS_ERR_INVALID_ARGUMENT, "unknown policy");
+  if (!kern) return fail(RS_ERR_INVALID_ARGUMENT, "unknown policy");
+  rs_status s2 = launch_kernel(kern, kp, best_wpb, block_smem, tr->num_replays, st);
+  if (s2 != RS_OK) return s2;
+  // nearest-rank percentiles (metrics.hpp:62-80), one CTA per replay
+  rs::StatsParams sp;
+  sp.num_replays = tr->num_replays;
+  sp.offsets = kp.offsets;
+  sp.arrival = kp.arrival;
+  sp.decode = kp.decode;
+  sp.first = kp.o_first;
+  sp.completion = kp.o_completion;
+  sp.stats = stats;
+  {
+    int sms = 0;
+    RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int grid = std::max(1, std::min(tr->num_replays, sms * 8));
+    rs::percentile_kernel<<<grid, rs::kStatsThreads, 0, st>>>(sp);
+    RS_CUDA(cudaGetLastError());
+  }
+  return RS_OK;
 }
 
 }  // extern "C"

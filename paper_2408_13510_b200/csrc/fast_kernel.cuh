@@ -249,6 +249,89 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
   }
 }
 
+// Fused predictor: the predictions of the 32 requests of the arrival window
+// [a_base, a_base + 32), drawn in index order from the replay's own
+// mt19937_64 stream exactly as inject_arrivals draws them (env.hpp:357-375,
+// predict_simulated predictor.hpp:98-110: one draw, a second for a miss in a
+// middle bucket).  The stream is policy independent, so drawing a window
+// ahead of injection is equivalent.  Written to the predicted-bucket output.
+__device__ inline void predict_window(const KParams& P, Replay& R, unsigned long long* pst, int l) {
+  const int j = R.a_base + l;
+  const bool v = j < R.n;
+  const long long g = R.off + j;
+  int pred = 0;
+  if (P.predictor_mode == RS_PREDICTOR_GIVEN) {
+    if (v) pred = P.given_bucket[g];
+  } else if (P.predictor_mode == RS_PREDICTOR_EMPIRICAL) {  // predictor.hpp:146-158
+    if (v) pred = P.emp_table[P.task[g]][bucket_of(P.band_edges, P.n_band_edges, P.prompt[g])];
+  } else {
+    const int nb = P.n_pred_edges;
+    int tb = 0;
+    double acc = 1.0;
+    if (v) {
+      tb = bucket_of(P.pred_edges, nb, P.decode[g]);
+      acc = P.accuracy[P.task[g]];
+    }
+    unsigned long long* ob = pst + 312;
+    const int cnt = min(kWarp, R.n - R.a_base);
+    for (int k = 0; k < cnt; ++k) {
+      const int tbk = __shfl_sync(kFull, tb, k);
+      const double ak = __shfl_sync(kFull, acc, k);
+      int pk = 0;
+      if (nb > 1) {
+        if (R.pred_pos == 312) {
+          mt_twist_warp(pst, l);
+          for (int q = l; q < 312; q += kWarp) ob[q] = mt_temper(pst[q]);
+          __syncwarp();
+          R.pred_pos = 0;
+        }
+        const double u = u01(ob[R.pred_pos++]);
+        if (u < ak) {
+          pk = tbk;
+        } else if (tbk == 0) {
+          pk = 1;
+        } else if (tbk == nb - 1) {
+          pk = nb - 2;
+        } else {
+          if (R.pred_pos == 312) {
+            mt_twist_warp(pst, l);
+            for (int q = l; q < 312; q += kWarp) ob[q] = mt_temper(pst[q]);
+            __syncwarp();
+            R.pred_pos = 0;
+          }
+          pk = u01(ob[R.pred_pos++]) < 0.5 ? tbk - 1 : tbk + 1;
+        }
+      }
+      if (l == k) pred = pk;
+    }
+  }
+  if (v) P.o_pred[g] = (uint8_t)pred;
+  __syncwarp();
+}
+
+__device__ __forceinline__ void load_window_fast(const KParams& P, Replay& R,
+                                                 unsigned long long* pst, int l) {
+  load_arrival_window(P, R, l);
+  if (P.predict_inline) predict_window(P, R, pst, l);
+}
+
+// ClusterSim::inject_arrivals (env.hpp:357-375): a cursor advance over the
+// register window of arrival times; the next window is predicted on load.
+__device__ __forceinline__ void inject_fast(const KParams& P, Replay& R, unsigned long long* pst,
+                                            int l) {
+  for (;;) {
+    const int j = R.a_base + l;
+    const bool ok = j >= R.cursor && j < R.n && R.a_val <= R.clock;
+    R.cursor += __popc(__ballot_sync(kFull, ok));
+    if (R.cursor == R.a_base + kWarp && R.cursor < R.n) {
+      R.a_base += kWarp;
+      load_window_fast(P, R, pst, l);
+      continue;
+    }
+    break;
+  }
+}
+
 // Returns true when the replay must be re-run instance-sequentially.
 template <int POL, int G>
 __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const MlpView& M, int r,
@@ -302,8 +385,12 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
   if (POL == RS_POLICY_RL && P.rl_eps > 0.0)
     mt_seed_warp(reinterpret_cast<unsigned long long*>(gbase + P.off_rng),
                  P.policy_seed ? P.policy_seed[r] : 0ull, l);
+  unsigned long long* pst = reinterpret_cast<unsigned long long*>(gbase + P.off_pred);
+  R.pred_pos = 312;
+  if (P.predict_inline && P.predictor_mode == RS_PREDICTOR_SIMULATED)
+    mt_seed_warp(pst, P.predictor_seed[r], l);  // Rng(predictor_seed), env.hpp:173
   __syncwarp();
-  load_arrival_window(P, R, l);
+  load_window_fast(P, R, pst, l);
   // arrival time of the next request to inject (+inf when none is left)
   auto next_arrival = [&]() {
     const int k = R.cursor - R.a_base;
@@ -314,7 +401,7 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
   R.hr_prompt = R.hr_true = R.hr_bucket = 0;
   if (bad) R.status = RS_REPLAY_INVALID_TRACE;
   else if (too_big) R.status = RS_REPLAY_CAPACITY;
-  else inject(P, R, l);
+  else inject_fast(P, R, pst, l);
   next_arrival();
 
   while (R.status == RS_REPLAY_FINISHED && R.completed != R.n && R.tick < P.max_ticks) {
@@ -528,7 +615,7 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
     }
     R.clock = t1;
     if (R.clock >= R.next_arr) {  // inject_arrivals (env.hpp:357-375) only when due
-      inject(P, R, l);
+      inject_fast(P, R, pst, l);
       next_arrival();
     }
     R.tick++;

@@ -200,7 +200,7 @@ rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, 
   dout.predicted_bucket = reinterpret_cast<uint8_t*>(b + o_pb);
   rs_replay_stats* dstats = reinterpret_cast<rs_replay_stats*>(b + o_st);
 
-  if ((s = forward(rs_predict_buckets(&dcfg, &dt, dout.predicted_bucket, st))) != RS_OK) return s;
+  dcfg.flags |= RS_FLAG_PREDICT_INLINE;  // predictions drawn inside the replay
   if ((s = forward(rs_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st))) != RS_OK)
     return s;
   auto d2h = [&](void* dst, size_t off, size_t n) -> cudaError_t {

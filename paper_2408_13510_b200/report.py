@@ -38,14 +38,27 @@ def summary(arrival, decode, routed, first, completion, preemptions, stats, num_
     has_tbt = dd >= 2
     tbt = (completion[done][has_tbt] - first[done][has_tbt]) / (dd[has_tbt] - 1).astype(np.float64)
     ticks = int(stats["ticks"])
+    if int(stats["percentiles_valid"]):
+        # device nearest-rank selections (percentile_kernel, stats.cuh)
+        def _dev(name, n, total):
+            return {"mean": total / n if n else 0.0, "p50": float(stats[f"{name}_p50"]),
+                    "p90": float(stats[f"{name}_p90"]), "p99": float(stats[f"{name}_p99"]),
+                    "count": int(n)}
+        e2e_agg = _dev("e2e", e2e.shape[0], float(stats["total_e2e_s"]))
+        ttft_agg = _dev("ttft", ttft.shape[0], float(stats["total_ttft_s"]))
+        tbt_agg = _dev("tbt", tbt.shape[0], float(stats["total_tbt_s"]))
+    else:
+        e2e_agg = _agg(e2e, float(stats["total_e2e_s"]))
+        ttft_agg = _agg(ttft, float(stats["total_ttft_s"]))
+        tbt_agg = _agg(tbt, float(stats["total_tbt_s"]))
     out = {
         "completed": int(stats["completed"]),
         "total_tokens": int(stats["total_tokens"]),
         "total_e2e_s": float(stats["total_e2e_s"]),
         "makespan_s": float(stats["makespan_s"]),
-        "e2e_s": _agg(e2e, float(stats["total_e2e_s"])),
-        "ttft_s": _agg(ttft, float(stats["total_ttft_s"])),
-        "tbt_s": _agg(tbt, float(stats["total_tbt_s"])),
+        "e2e_s": e2e_agg,
+        "ttft_s": ttft_agg,
+        "tbt_s": tbt_agg,
         "mean_router_wait_s": (float(stats["total_router_wait_s"]) / int(done.sum())
                                if done.any() else 0.0),
         "mean_router_queue": float(stats["sum_router_queue"]) / ticks if ticks else 0.0,

@@ -217,8 +217,11 @@ def compare(a: ReplayResult, b: ReplayResult, exact_times: bool = True) -> list[
               "sum_instance_waiting"):
         if sa[f] != sb[f]:
             errs.append(f"stats.{f}: {sa[f]} vs {sb[f]}")
+    pct = ("e2e_p50", "e2e_p90", "e2e_p99", "ttft_p50", "ttft_p90", "ttft_p99", "tbt_p50",
+           "tbt_p90", "tbt_p99")
+    both_pct = sa["percentiles_valid"] and sb["percentiles_valid"]
     for f in ("clock", "total_e2e_s", "total_ttft_s", "total_tbt_s", "total_router_wait_s",
-              "makespan_s"):
+              "makespan_s") + (pct if both_pct else ()):
         x, y = float(sa[f]), float(sb[f])
         if exact_times and not (x == y or (np.isnan(x) and np.isnan(y))):
             errs.append(f"stats.{f}: {x!r} vs {y!r}")
