@@ -215,11 +215,20 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2408_13510_b200 import abi, engine
+    from paper_2408_13510_b200 import dist as rdist
 
     rank, world, local = dist_env()
+    # RS_BENCH_SAME_DEVICE / RS_DIST_BACKEND=gloo exist only to exercise the
+    # multi-rank path on a one-GPU box; the real run is one rank per GPU on NCCL.
+    if os.environ.get("RS_BENCH_SAME_DEVICE"):
+        local = 0
+    backend = os.environ.get("RS_DIST_BACKEND", "nccl")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     lib = abi.load_library()
     if lib.rs_device_count() < 1:
         raise RuntimeError("no sm_100 device")
@@ -273,7 +282,10 @@ def main():
         if ev is not None:
             ev[1].record(stream)
         if world > 1:  # final gather of the per-replay statistics (NCCL)
-            dist.all_gather_into_tensor(gathered, d_st)
+            if backend == "nccl":
+                dist.all_gather_into_tensor(gathered, d_st)
+            else:  # gloo gathers host tensors
+                gathered.copy_(rdist.gather_stats(d_st.cpu(), world))
 
     # Pre-warm: a fresh box's first seconds of work run ~35% slower (clock /
     # power ramp; measured), so repeat untimed full steps for >= PREWARM_S
@@ -304,15 +316,9 @@ def main():
             dist.barrier()
     elapsed = start.elapsed_time(stop) / 1e3
     replay_s = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3 / args.steps
-    t = torch.tensor([elapsed, float(ticks_local)], dtype=torch.float64, device=dev)
-    if world > 1:
-        mx = t.clone()
-        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
-        sm = t.clone()
-        dist.all_reduce(sm[1:], op=dist.ReduceOp.SUM)
-        elapsed, ticks_total = float(mx[0]), float(sm[1])
-    else:
-        ticks_total = float(ticks_local)
+    red_dev = dev if backend == "nccl" else "cpu"
+    elapsed = rdist.max_over_ranks(elapsed, red_dev)          # slowest rank's device time
+    ticks_total = rdist.sum_over_ranks(float(ticks_local), red_dev)
     value = ticks_total * args.steps / elapsed
 
     # ------------------------------------------------------------ e2e (C ABI)
@@ -347,10 +353,7 @@ def main():
             for _ in range(args.steps):
                 e2e_step()
             torch.cuda.synchronize(dev)
-            te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-            if world > 1:
-                dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            return float(te[0])
+            return rdist.max_over_ranks(time.perf_counter() - t0, red_dev)
 
         # headline e2e: the reference-facing result of evaluate_policy
         # (experiment.hpp:648-670) is the per-replay statistics, so the D2H
@@ -381,7 +384,10 @@ def main():
     prof = ROOT / "profiles" / f"ncu_replay_{args.config}.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            pj = json.loads(prof.read_text())
+            # only when the profiled launch had this exact shape
+            if pj.get("algorithmic_bytes_per_launch") == alg_bytes:
+                traffic = pj.get("dram_bytes_per_launch")
         except (ValueError, OSError):
             traffic = None
     line = {

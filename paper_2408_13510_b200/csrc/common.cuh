@@ -125,7 +125,26 @@ struct KParams {
   int off_pred;                    // mt19937_64 state + 312 outputs (bytes)
   const uint64_t* predictor_seed;
   const uint8_t* given_bucket;
+  // streamed inputs (host entry point): requests [0, *resident) of every
+  // replay are on the device; the copy stream raises it chunk by chunk while
+  // the replay runs (nullptr = everything resident, validated up front)
+  const int* resident;
 };
+
+// acquire-load of the streamed-input watermark
+constexpr unsigned long long kStreamTimeoutNs = 20000000000ull;  // 20 s
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ int load_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // x / c, correctly rounded; a multiply when c is a power of two.
 __device__ __forceinline__ double div_exact(double x, double c, double inv_c, int pow2) {

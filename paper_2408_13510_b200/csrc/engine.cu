@@ -20,6 +20,7 @@
 #include "router.cuh"
 #include "fast_kernel.cuh"
 #include "stats.cuh"
+#include "internal.h"
 
 namespace {
 
@@ -434,6 +435,26 @@ rs_status rs_predict_buckets(const rs_batch_cfg* cfg, const rs_trace_soa* tr,
 rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_out* out,
                           rs_replay_stats* stats, void* workspace, size_t workspace_bytes,
                           void* stream) {
+  return rs_internal_replay_batch(cfg, tr, out, stats, workspace, workspace_bytes, stream,
+                                  nullptr, nullptr);
+}
+
+}  // extern "C"
+
+// Streamed-input variant (used by rs_replay_batch_host): requests
+// [0, *resident) of every replay are on the device, the rest still in flight
+// on a copy stream that bumps *resident; the lane-per-instance kernel gates
+// each 32-request arrival window on it. `inputs_done` (recorded by the copy
+// stream after its last chunk) orders the percentile pass after the copies.
+bool rs_internal_fast_path(const rs_batch_cfg* cfg) {
+  return cfg->chunk_size == 0 && cfg->num_instances <= 64 &&
+         env_int("RS_FORCE_GENERAL", 0) == 0;
+}
+
+rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr,
+                                   rs_req_out* out, rs_replay_stats* stats, void* workspace,
+                                   size_t workspace_bytes, void* stream, const int* resident,
+                                   void* inputs_done) {
   rs_status s = validate(cfg);
   if (s != RS_OK) return s;
   if ((s = require_device()) != RS_OK) return s;
@@ -459,7 +480,9 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
   const int wcap = std::max(8, std::min(128, env_int("RS_WAIT_RING", wdef)));
   // whole-prompt prefill (no chunking, m <= 64) takes the lane-per-instance
   // kernel; chunked prefill and larger fleets take the general kernel
-  const bool fast = cfg->chunk_size == 0 && m_inst <= 64 && env_int("RS_FORCE_GENERAL", 0) == 0;
+  const bool fast = rs_internal_fast_path(cfg);
+  if (resident && !fast)
+    return fail(RS_ERR_INVALID_ARGUMENT, "streamed inputs need the lane-per-instance kernel");
   const int groups = m_inst <= 32 ? 1 : 2;
   Layout L = make_layout(*cfg, wcap, fast);
   rs::KParams kp;
@@ -535,6 +558,7 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
   kp.off_pred = L.off_pred;
   kp.predictor_seed = tr->predictor_seed;
   kp.given_bucket = tr->given_bucket;
+  kp.resident = resident;
   if (cfg->flags & RS_FLAG_PREDICT_INLINE) {
     if (cfg->predictor_mode == RS_PREDICTOR_SIMULATED && !tr->predictor_seed)
       return fail(RS_ERR_INVALID_ARGUMENT, "simulated predictor needs trace->predictor_seed");
@@ -651,6 +675,7 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
   rs_status s2 = launch_kernel(kern, kp, best_wpb, block_smem, tr->num_replays, st);
   if (s2 != RS_OK) return s2;
   // nearest-rank percentiles (metrics.hpp:62-80), one CTA per replay
+  if (inputs_done) RS_CUDA(cudaStreamWaitEvent(st, (cudaEvent_t)inputs_done, 0));
   rs::StatsParams sp;
   sp.num_replays = tr->num_replays;
   sp.offsets = kp.offsets;
@@ -669,4 +694,3 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_re
   return RS_OK;
 }
 
-}  // extern "C"

@@ -311,7 +311,50 @@ __device__ inline void predict_window(const KParams& P, Replay& R, unsigned long
 
 __device__ __forceinline__ void load_window_fast(const KParams& P, Replay& R,
                                                  unsigned long long* pst, int l) {
-  load_arrival_window(P, R, l);
+  if (P.resident) {
+    // streamed inputs: wait until the copy stream has landed this window
+    const int need = min(R.n, R.a_base + kWarp);
+    if (need > R.resident_seen) {
+      // every lane acquires; the warp minimum is visible to all of them
+      int v = __reduce_min_sync(kFull, load_acquire(P.resident));
+      if (v < need) {
+        const unsigned long long t0 = globaltimer_ns();
+        while (v < need) {
+          __nanosleep(256);
+          v = __reduce_min_sync(kFull, load_acquire(P.resident));
+          if (v < need && __any_sync(kFull, globaltimer_ns() - t0 > kStreamTimeoutNs)) {
+            R.status = RS_REPLAY_NOT_RUN;  // copy stream never delivered
+            return;
+          }
+        }
+      }
+      R.resident_seen = v;
+    }
+    const double prev_last = __shfl_sync(kFull, R.a_val, kWarp - 1);
+    load_arrival_window(P, R, l);
+    // lazy validation of the window (the up-front pass cannot read inputs
+    // that are still in flight): arrivals non-decreasing, token ranges, and
+    // the 32-bit aggregate bound over the requests seen so far
+    const int j = R.a_base + l;
+    const bool v = j < R.n;
+    bool bad = false;
+    int vm = 0;
+    if (v) {
+      const long long g = R.off + j;
+      const int p = P.prompt[g], d = P.decode[g];
+      bad = p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens;
+      vm = p + (d > P.ub_max ? d : P.ub_max);
+    }
+    const double up = __shfl_up_sync(kFull, R.a_val, 1);
+    const double prev = l == 0 ? prev_last : up;
+    if (v && j > 0 && R.a_val < prev) bad = true;
+    vm = warp_max(vm);
+    R.vmax = vm > R.vmax ? vm : R.vmax;
+    if (__any_sync(kFull, bad)) R.status = RS_REPLAY_INVALID_TRACE;
+    else if ((long long)R.n * R.vmax > (1ll << 30)) R.status = RS_REPLAY_CAPACITY;
+  } else {
+    load_arrival_window(P, R, l);
+  }
   if (P.predict_inline) predict_window(P, R, pst, l);
 }
 
@@ -326,6 +369,7 @@ __device__ __forceinline__ void inject_fast(const KParams& P, Replay& R, unsigne
     if (R.cursor == R.a_base + kWarp && R.cursor < R.n) {
       R.a_base += kWarp;
       load_window_fast(P, R, pst, l);
+      if (R.status != RS_REPLAY_FINISHED) break;  // streamed window failed validation
       continue;
     }
     break;
@@ -353,6 +397,7 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
     P.o_completion[g] = -1.0;
     P.o_preempt[g] = 0;
     if (POL == RS_POLICY_MIN_MIN) P.mm_removed[g] = 0;
+    if (P.resident) continue;  // streamed inputs: validated per window on load
     const int p = P.prompt[g], d = P.decode[g];
     if (p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens) bad = true;
     if (j > 0 && P.arrival[g] < P.arrival[g - 1]) bad = true;
@@ -387,6 +432,8 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
                  P.policy_seed ? P.policy_seed[r] : 0ull, l);
   unsigned long long* pst = reinterpret_cast<unsigned long long*>(gbase + P.off_pred);
   R.pred_pos = 312;
+  R.a_val = 0.0;
+  R.resident_seen = R.vmax = 0;
   if (P.predict_inline && P.predictor_mode == RS_PREDICTOR_SIMULATED)
     mt_seed_warp(pst, P.predictor_seed[r], l);  // Rng(predictor_seed), env.hpp:173
   __syncwarp();
@@ -401,7 +448,7 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
   R.hr_prompt = R.hr_true = R.hr_bucket = 0;
   if (bad) R.status = RS_REPLAY_INVALID_TRACE;
   else if (too_big) R.status = RS_REPLAY_CAPACITY;
-  else inject_fast(P, R, pst, l);
+  else if (R.status == RS_REPLAY_FINISHED) inject_fast(P, R, pst, l);
   next_arrival();
 
   while (R.status == RS_REPLAY_FINISHED && R.completed != R.n && R.tick < P.max_ticks) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -11,6 +12,7 @@
 
 #include "../../include/rs_abi.h"
 #include "common.cuh"
+#include "internal.h"
 #include "mlp.cuh"
 
 namespace rs {
@@ -41,6 +43,10 @@ struct DeviceCache {
   void* base = nullptr;
   size_t bytes = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;      // streamed inputs (rs_replay_batch_host)
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+  int* marks = nullptr;                    // pinned residency watermarks
+  int nmarks = 0;
 };
 DeviceCache g_cache[16];
 
@@ -161,6 +167,7 @@ rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, 
   const size_t o_pb = o; o += al(1ull * N);
   const size_t o_st = o; o += al(sizeof(rs_replay_stats) * R);
   const size_t o_ws = o; o += al(ws_bytes);
+  const size_t o_fl = o; o += al(4);
   DeviceCache& dc = g_cache[device];
   std::lock_guard<std::mutex> lock(dc.mu);
   char* b = nullptr;
@@ -170,11 +177,25 @@ rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, 
     if (!src || n == 0) return cudaSuccess;
     return cudaMemcpyAsync(b + off, src, n, cudaMemcpyHostToDevice, st);
   };
+  // Streamed inputs: when every replay has the same length n and the input
+  // is large, the per-request arrays travel in arrival-index chunks on a copy
+  // stream while the replay kernel runs; after each chunk the copy stream
+  // raises a device watermark (a 4-byte copy from pinned memory, ordered
+  // behind the chunk) that the kernel waits on per 32-request window.
+  const int64_t n_eq = N / R;
+  bool uniform = N % R == 0;
+  for (int r = 0; uniform && r < R; ++r) uniform = tr->offsets[r + 1] - tr->offsets[r] == n_eq;
+  const char* se = getenv("RS_STREAM_INPUTS");
+  const int64_t min_stream = se ? atoll(se) : (int64_t)1 << 22;
+  const bool stream_in = uniform && n_eq > 0 && min_stream > 0 && N >= min_stream &&
+                         rs_internal_fast_path(cfg);
   RS_CUDA2(h2d(o_off, tr->offsets, 8ull * (R + 1)));
-  RS_CUDA2(h2d(o_arr, tr->arrival_s, 8ull * N));
-  RS_CUDA2(h2d(o_pr, tr->prompt_tokens, 4ull * N));
-  RS_CUDA2(h2d(o_de, tr->decode_tokens, 4ull * N));
-  RS_CUDA2(h2d(o_tk, tr->task, 1ull * N));
+  if (!stream_in) {
+    RS_CUDA2(h2d(o_arr, tr->arrival_s, 8ull * N));
+    RS_CUDA2(h2d(o_pr, tr->prompt_tokens, 4ull * N));
+    RS_CUDA2(h2d(o_de, tr->decode_tokens, 4ull * N));
+    RS_CUDA2(h2d(o_tk, tr->task, 1ull * N));
+  }
   if (tr->given_bucket) RS_CUDA2(h2d(o_gv, tr->given_bucket, 1ull * N));
   if (tr->predictor_seed) RS_CUDA2(h2d(o_ps, tr->predictor_seed, 8ull * R));
   if (tr->policy_seed) RS_CUDA2(h2d(o_qs, tr->policy_seed, 8ull * R));
@@ -201,8 +222,61 @@ rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, 
   rs_replay_stats* dstats = reinterpret_cast<rs_replay_stats*>(b + o_st);
 
   dcfg.flags |= RS_FLAG_PREDICT_INLINE;  // predictions drawn inside the replay
-  if ((s = forward(rs_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st))) != RS_OK)
-    return s;
+  if (!stream_in) {
+    if ((s = forward(rs_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st))) !=
+        RS_OK)
+      return s;
+  } else {
+    // chunk boundaries: small first chunk (the kernel starts on it), doubling
+    std::vector<int> bounds;
+    for (int64_t e = std::min<int64_t>(n_eq, 128); ; e = std::min<int64_t>(n_eq, 2 * e)) {
+      bounds.push_back((int)e);
+      if (e == n_eq) break;
+    }
+    if (!dc.copy_stream)
+      RS_CUDA2(cudaStreamCreateWithFlags(&dc.copy_stream, cudaStreamNonBlocking));
+    if (!dc.ev_ready) RS_CUDA2(cudaEventCreateWithFlags(&dc.ev_ready, cudaEventDisableTiming));
+    if (!dc.ev_done) RS_CUDA2(cudaEventCreateWithFlags(&dc.ev_done, cudaEventDisableTiming));
+    if (dc.nmarks < (int)bounds.size()) {
+      if (dc.marks) cudaFreeHost(dc.marks);
+      dc.marks = nullptr;
+      dc.nmarks = 0;
+      RS_CUDA2(cudaMallocHost(&dc.marks, sizeof(int) * bounds.size()));
+      dc.nmarks = (int)bounds.size();
+    }
+    for (size_t i = 0; i < bounds.size(); ++i) dc.marks[i] = bounds[i];
+    int* flag = reinterpret_cast<int*>(b + o_fl);
+    RS_CUDA2(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    RS_CUDA2(cudaEventRecord(dc.ev_ready, st));
+    const cudaStream_t cs = dc.copy_stream;
+    RS_CUDA2(cudaStreamWaitEvent(cs, dc.ev_ready, 0));
+    // the copy stream is queued first (it only waits for the flag reset);
+    // the replay kernel then runs concurrently with it
+    struct Col { size_t off; const void* src; size_t es; };
+    const Col cols[4] = {{o_arr, tr->arrival_s, 8}, {o_pr, tr->prompt_tokens, 4},
+                         {o_de, tr->decode_tokens, 4}, {o_tk, tr->task, 1}};
+    int lo = 0;
+    for (size_t i = 0; i < bounds.size(); ++i) {
+      const int hi = bounds[i];
+      for (const Col& c : cols) {
+        if (!c.src) continue;
+        const size_t pitch = (size_t)n_eq * c.es;
+        RS_CUDA2(cudaMemcpy2DAsync(b + c.off + (size_t)lo * c.es, pitch,
+                                   static_cast<const char*>(c.src) + (size_t)lo * c.es, pitch,
+                                   (size_t)(hi - lo) * c.es, (size_t)R, cudaMemcpyHostToDevice,
+                                   cs));
+      }
+      RS_CUDA2(cudaMemcpyAsync(flag, dc.marks + i, sizeof(int), cudaMemcpyHostToDevice, cs));
+      lo = hi;
+    }
+    RS_CUDA2(cudaEventRecord(dc.ev_done, cs));
+    s = forward(rs_internal_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st, flag,
+                                         dc.ev_done));
+    if (s != RS_OK) {
+      cudaStreamSynchronize(cs);
+      return s;
+    }
+  }
   auto d2h = [&](void* dst, size_t off, size_t n) -> cudaError_t {
     if (!dst || n == 0) return cudaSuccess;
     return cudaMemcpyAsync(dst, b + off, n, cudaMemcpyDeviceToHost, st);

@@ -1,0 +1,17 @@
+// Engine-internal entry points shared between engine.cu and host_api.cu
+// (not part of the C ABI in include/rs_abi.h).
+#pragma once
+#include "../../include/rs_abi.h"
+
+// true when `cfg` runs on the lane-per-instance kernel (whole-prompt
+// prefill, <= 64 instances), the only kernel that accepts streamed inputs
+bool rs_internal_fast_path(const rs_batch_cfg* cfg);
+
+// rs_replay_batch with optional streamed inputs: `resident` (device int,
+// may be null) counts the requests of every replay already on the device;
+// `inputs_done` (cudaEvent_t, may be null) is waited on before the
+// percentile pass.
+rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr,
+                                   rs_req_out* out, rs_replay_stats* stats, void* workspace,
+                                   size_t workspace_bytes, void* stream, const int* resident,
+                                   void* inputs_done);

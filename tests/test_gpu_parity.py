@@ -18,14 +18,17 @@ pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
-@pytest.fixture(params=["fast", "general"], autouse=True)
+@pytest.fixture(params=["fast", "general", "streamed"], autouse=True)
 def kernel_path(request, monkeypatch):
     """Every parity test runs on both replay kernels: the lane-per-instance
-    fast kernel (whole-prompt prefill) and the general warp-per-instance one."""
+    fast kernel (whole-prompt prefill) and the general warp-per-instance one;
+    "streamed" forces rs_replay_batch_host's chunked input copies overlapping
+    the fast kernel (taken whenever the replays have equal lengths)."""
     if request.param == "general":
         monkeypatch.setenv("RS_FORCE_GENERAL", "1")
     else:
         monkeypatch.delenv("RS_FORCE_GENERAL", raising=False)
+    monkeypatch.setenv("RS_STREAM_INPUTS", "1" if request.param == "streamed" else "0")
     return request.param
 
 
@@ -244,3 +247,22 @@ def test_conservation_properties_at_scale(gpu):
     res2 = sim.run_policy("workload_aware")
     assert np.array_equal(res.stats["decision_hash"], res2.stats["decision_hash"])
     assert np.array_equal(res.completion.view(np.uint64), res2.completion.view(np.uint64))
+
+
+def test_streamed_inputs_validate_per_window(gpu, kernel_path):
+    # Streamed inputs are validated as each 32-request window lands: a bad
+    # request deep in one replay fails that replay only.
+    if kernel_path != "streamed":
+        pytest.skip("streamed-input path only")
+    tb = engine.build_workload([5, 6, 7], 3000, 20.0)
+    traces = [O.Trace(tb.arrival[tb.replay(r)].copy(), tb.prompt[tb.replay(r)].copy(),
+                      tb.decode[tb.replay(r)].copy(), tb.task[tb.replay(r)].copy())
+              for r in range(3)]
+    traces[1].arrival[2500] = traces[1].arrival[2499] - 1.0  # arrivals out of order
+    traces[2].prompt[1700] = 0                                # empty prompt
+    ps = [abi.mix_seed(s, 0x9DED) for s in (5, 6, 7)]
+    cfg = abi.default_config("workload_aware", 4)
+    got = run_engine(gpu, cfg, traces, ps)
+    assert O.compare(got[0], O.ora_run(cfg, traces[0], ps[0])) == []
+    assert got[1].stats["status"][0] == abi.REPLAY_INVALID_TRACE
+    assert got[2].stats["status"][0] == abi.REPLAY_INVALID_TRACE
