@@ -44,7 +44,7 @@ REPLAY_BYTES_PER_REPLAY = 8 + 256  # offsets + stats record
 PREWARM_S = 2.0
 
 CONFIGS = {
-    # name: (requests, replays per GPU, instances, rate, policy, weights, description)
+    # name: (requests, seeds per GPU, instances, rate(s), policy (or policies), weights, description)
     "c1": (2000, 1, 4, 20.0, "workload_aware", None,
            "c1: single 2,000-request 5-task-mix trace (lambda=20), 4 instances, workload_aware"),
     "c2": (31329, 1024, 8, 20.0, "workload_aware", None,
@@ -53,10 +53,23 @@ CONFIGS = {
     "c3": (4000, 4096, 8, 40.0, "rl", None,
            "c3: RL Q-network (51-64-64-9, random init seed 42) greedy rollouts, 4,096 replays x "
            "4,000 requests (lambda=40), 8 instances"),
+    "c4": (2000, 1024, 4, tuple(5.0 * k for k in range(1, 17)),
+           ("round_robin", "jsq", "workload_aware", "rl"), None,
+           "c4: policy sweep {round_robin, jsq, workload_aware, rl (27-64-64-5, random init "
+           "seed 42)} x 16 arrival rates (lambda=5..80) x 1,024 seeds per GPU, 2,000-request "
+           "traces, 4 instances (65,536 replays per GPU per step)"),
     "c5": (200000, 512, 64, 40.0, "workload_aware", (0.0, 3.0, 1.0, 2.0, 0.0),
            "c5: 64 instances, 200k-request heavy-decode mixture (weights 0/3/1/2/0, lambda=40) "
            "x 512 seeds per GPU"),
 }
+
+
+def cfg_shape(cfgname):
+    """(requests, seeds per GPU, instances, rates, policies, weights, description)."""
+    n, R, m, rate, pol, w, desc = CONFIGS[cfgname]
+    rates = tuple(rate) if isinstance(rate, tuple) else (rate,)
+    pols = tuple(pol) if isinstance(pol, tuple) else (pol,)
+    return n, R, m, rates, pols, w, desc
 
 
 def dist_env():
@@ -121,12 +134,22 @@ class ClockSampler:
 
 
 def make_workload(cfgname, rank, threads=0):
+    """The config's traces on this rank: for every arrival rate, seeds
+    rank*R+1..(rank+1)*R (one replay each), rate-major.  Every policy of a
+    sweep replays the same traces."""
     from paper_2408_13510_b200 import abi, engine
-    n, R, m, rate, policy, weights, desc = CONFIGS[cfgname]
+    n, R, m, rates, pols, weights, desc = cfg_shape(cfgname)
     seeds = np.arange(rank * R + 1, rank * R + R + 1, dtype=np.uint64)
-    tb = engine.build_workload(seeds, n, rate, weights, threads=threads)
-    pseeds = np.array([abi.mix_seed(int(s), 0x9DED) for s in seeds], np.uint64)
-    return tb, pseeds, seeds
+    parts = [engine.build_workload(seeds, n, rate, weights, threads=threads) for rate in rates]
+    if len(parts) == 1:
+        tb = parts[0]
+    else:
+        cat = lambda f: np.ascontiguousarray(np.concatenate([getattr(t, f) for t in parts]))
+        off = np.arange(len(parts) * R + 1, dtype=np.int64) * n
+        tb = engine.TraceBatch(off, cat("arrival"), cat("prompt"), cat("decode"), cat("task"))
+    all_seeds = np.tile(seeds, len(rates))
+    pseeds = np.array([abi.mix_seed(int(s), 0x9DED) for s in all_seeds], np.uint64)
+    return tb, pseeds, all_seeds
 
 
 def agent_for(m):
@@ -138,31 +161,44 @@ def agent_for(m):
 
 
 def cpu_reference(cfgname, sample_replays, threads):
-    """Compiled unmodified reference (oracle/_ref) on host threads."""
+    """Compiled unmodified reference (oracle/_ref) on host threads: a bounded
+    sample of the config's replays (for a sweep, spread over its policies
+    and arrival rates).  Returns (decisions/s, decisions, wall s, description)."""
     sys.path.insert(0, str(ROOT / "tests"))
     import oracles as O  # baseline infrastructure
-    from paper_2408_13510_b200 import abi
-    n, R, m, rate, policy, weights, desc = CONFIGS[cfgname]
+    from paper_2408_13510_b200 import abi, engine
+    n, R, m, rates, pols, weights, desc = cfg_shape(cfgname)
     lib = O.ref_lib()
-    seeds = np.arange(1, sample_replays + 1, dtype=np.uint64)
-    from paper_2408_13510_b200 import engine
-    tb = engine.build_workload(seeds, n, rate, weights, threads=threads)
-    ps = np.array([abi.mix_seed(int(s), 0x9DED) for s in seeds], np.uint64)
-    cfg = abi.default_config(policy, m)
-    keep = None
-    if policy == "rl":
-        dims, params = agent_for(m)
-        keep = abi.set_rl(cfg, dims, params)
-    stats = np.zeros(sample_replays, abi.STATS_DTYPE)
-    wall = lib.ref_run_batch(C.byref(cfg), sample_replays, tb.offsets.ctypes.data,
-                             tb.arrival.ctypes.data, tb.prompt.ctypes.data, tb.decode.ctypes.data,
-                             tb.task.ctypes.data, ps.ctypes.data, None, threads,
-                             stats.ctypes.data)
-    del keep
-    if wall <= 0:
-        raise RuntimeError("reference batch failed: " + O.ref_error())
-    ticks = int(stats["ticks"].sum())
-    return ticks / wall, ticks, wall
+    per = max(1, sample_replays)  # one replay per host thread, per policy
+    ticks = 0
+    wall = 0.0
+    for pi, policy in enumerate(pols):
+        # this policy's sample: seeds 1..per, rates spread over the sweep
+        pick = [rates[(pi + k * max(1, len(rates) // per)) % len(rates)] for k in range(per)]
+        parts = [engine.build_workload([k + 1], n, rate, weights) for k, rate in enumerate(pick)]
+        tb = engine.TraceBatch(np.arange(per + 1, dtype=np.int64) * n,
+                               np.concatenate([t.arrival for t in parts]),
+                               np.concatenate([t.prompt for t in parts]),
+                               np.concatenate([t.decode for t in parts]),
+                               np.concatenate([t.task for t in parts]))
+        ps = np.array([abi.mix_seed(k + 1, 0x9DED) for k in range(per)], np.uint64)
+        cfg = abi.default_config(policy, m)
+        keep = None
+        if policy == "rl":
+            dims, params = agent_for(m)
+            keep = abi.set_rl(cfg, dims, params)
+        stats = np.zeros(per, abi.STATS_DTYPE)
+        w = lib.ref_run_batch(C.byref(cfg), per, tb.offsets.ctypes.data, tb.arrival.ctypes.data,
+                              tb.prompt.ctypes.data, tb.decode.ctypes.data, tb.task.ctypes.data,
+                              ps.ctypes.data, None, threads, stats.ctypes.data)
+        del keep
+        if w <= 0:
+            raise RuntimeError("reference batch failed: " + O.ref_error())
+        ticks += int(stats["ticks"].sum())
+        wall += w
+    what = (f"{per} replays (seeds 1..{per}) per policy x {len(pols)} "
+            f"{'policies' if len(pols) > 1 else 'policy'} of the {cfgname} workload")
+    return ticks / wall, ticks, wall, what
 
 
 def run_reference_impl(args, cfgname):
@@ -170,24 +206,23 @@ def run_reference_impl(args, cfgname):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n, R, m, rate, policy, weights, desc = CONFIGS[cfgname]
+    n, R, m, rates, pols, weights, desc = cfg_shape(cfgname)
     sample = threads
-    rates = []
+    runs = []
     for i in range(args.warmup + args.steps):
-        v, ticks, wall = cpu_reference(cfgname, sample, threads)
+        v, ticks, wall, what = cpu_reference(cfgname, sample, threads)
         if i >= args.warmup:
-            rates.append((v, wall))
-    value = float(np.mean([r[0] for r in rates]))
+            runs.append((v, wall))
+    value = float(np.mean([r[0] for r in runs]))
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": float(np.mean([r[1] for r in rates]) * 1e3),
+            "ms_per_step": float(np.mean([r[1] for r in runs]) * 1e3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference workload generator)",
-            "config": {"workload": desc, "policy": policy, "instances": m,
+            "config": {"workload": desc, "policy": "+".join(pols), "instances": m,
                        "requests_per_replay": n},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"{sample} replays (seeds 1..{sample}) of the {cfgname} "
-                                       f"workload, one per host thread, per step"},
+                             "sample": f"{what}, one replay per host thread, per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -200,7 +235,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
-    ap.add_argument("--replays", type=int, default=0, help="override replays per GPU")
+    ap.add_argument("--replays", type=int, default=0, help="override seeds per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -232,11 +267,11 @@ def main():
     lib = abi.load_library()
     if lib.rs_device_count() < 1:
         raise RuntimeError("no sm_100 device")
-    n, R, m, rate, policy, weights, desc = CONFIGS[args.config]
+    n, R_seeds, m, rates, pols, weights, desc = cfg_shape(args.config)
     t_gen = time.time()
     tb, pseeds, seeds = make_workload(args.config, rank)
     t_gen = time.time() - t_gen
-    N = tb.total
+    N, R = tb.total, tb.num_replays
     dev = torch.device("cuda", local)
     tt = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     d_off, d_arr, d_pr, d_de, d_tk = (tt(tb.offsets), tt(tb.arrival), tt(tb.prompt),
@@ -248,44 +283,52 @@ def main():
     o_co = torch.empty(N, dtype=torch.float64, device=dev)
     o_pe = torch.empty(N, dtype=torch.int32, device=dev)
     o_pb = torch.empty(N, dtype=torch.uint8, device=dev)
-    d_st = torch.zeros(R * 256, dtype=torch.uint8, device=dev)
-    cfg = abi.default_config(policy, m)
-    keep = None
-    if policy == "rl":
-        dims, params = agent_for(m)
-        d_params = tt(params)
-        keep = abi.set_rl(cfg, dims, params)  # host copy for the e2e call
-        dcfg = abi.BatchCfg.from_buffer_copy(bytes(cfg))
-        dcfg.rl_params = C.cast(C.c_void_p(d_params.data_ptr()), C.POINTER(C.c_double))
-    else:
-        dcfg = cfg
-    ws_bytes = C.c_size_t(0)
-    abi.check(lib, lib.rs_workspace_size(C.byref(dcfg), R, N, C.byref(ws_bytes)))
-    d_ws = torch.empty(ws_bytes.value, dtype=torch.uint8, device=dev)
     tr = abi.TraceSoA(R, 0, N, d_off.data_ptr(), d_arr.data_ptr(), d_pr.data_ptr(),
                       d_de.data_ptr(), d_tk.data_ptr(), None, d_ps.data_ptr(), None)
     out = abi.ReqOut(o_in.data_ptr(), o_ro.data_ptr(), o_fi.data_ptr(), o_co.data_ptr(),
                      o_pe.data_ptr(), o_pb.data_ptr())
+
+    # one cell per policy: the same traces, the policy's config, its own stats
+    keep = []
+    cells = []
+    ws_max = 0
+    for policy in pols:
+        cfg = abi.default_config(policy, m)
+        if policy == "rl":
+            dims, params = agent_for(m)
+            d_params = tt(params)
+            keep += [abi.set_rl(cfg, dims, params), d_params]  # host copy for the e2e call
+            dcfg = abi.BatchCfg.from_buffer_copy(bytes(cfg))
+            dcfg.rl_params = C.cast(C.c_void_p(d_params.data_ptr()), C.POINTER(C.c_double))
+        else:
+            dcfg = abi.BatchCfg.from_buffer_copy(bytes(cfg))
+        dcfg.flags |= abi.RS_FLAG_PREDICT_INLINE  # predictor fused into the replay kernel
+        wsz = C.c_size_t(0)
+        abi.check(lib, lib.rs_workspace_size(C.byref(dcfg), R, N, C.byref(wsz)))
+        ws_max = max(ws_max, wsz.value)
+        cells.append({"policy": policy, "cfg": cfg, "dcfg": dcfg,
+                      "st": torch.zeros(R * 256, dtype=torch.uint8, device=dev)})
+    d_ws = torch.empty(ws_max, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     sh = stream.cuda_stream
     gathered = torch.empty(world * R * 256, dtype=torch.uint8, device=dev) if world > 1 else None
 
-    dcfg.flags |= abi.RS_FLAG_PREDICT_INLINE  # predictor fused into the replay kernel
-
     def step(ev=None):
-        # one rs_replay_batch = the replay kernel (predictions drawn at
-        # injection) + the per-replay percentile kernel, on torch's stream
+        # per cell one rs_replay_batch = the replay kernel (predictions drawn
+        # at injection) + the per-replay percentile kernel, on torch's stream
+        for k, c in enumerate(cells):
+            if ev is not None:
+                ev[k].record(stream)
+            abi.check(lib, lib.rs_replay_batch(C.byref(c["dcfg"]), C.byref(tr), C.byref(out),
+                                               c["st"].data_ptr(), d_ws.data_ptr(), ws_max, sh))
         if ev is not None:
-            ev[0].record(stream)
-        abi.check(lib, lib.rs_replay_batch(C.byref(dcfg), C.byref(tr), C.byref(out),
-                                           d_st.data_ptr(), d_ws.data_ptr(), ws_bytes.value, sh))
-        if ev is not None:
-            ev[1].record(stream)
+            ev[len(cells)].record(stream)
         if world > 1:  # final gather of the per-replay statistics (NCCL)
-            if backend == "nccl":
-                dist.all_gather_into_tensor(gathered, d_st)
-            else:  # gloo gathers host tensors
-                gathered.copy_(rdist.gather_stats(d_st.cpu(), world))
+            for c in cells:
+                if backend == "nccl":
+                    dist.all_gather_into_tensor(gathered, c["st"])
+                else:  # gloo gathers host tensors
+                    gathered.copy_(rdist.gather_stats(c["st"].cpu(), world))
 
     # Pre-warm: a fresh box's first seconds of work run ~35% slower (clock /
     # power ramp; measured), so repeat untimed full steps for >= PREWARM_S
@@ -297,11 +340,13 @@ def main():
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(dev)
-    stats = np.frombuffer(d_st.cpu().numpy().tobytes(), dtype=abi.STATS_DTYPE)
-    ticks_local = int(stats["ticks"].sum())
-    unfinished = int((stats["status"] != abi.REPLAY_FINISHED).sum())
+    cell_stats = [np.frombuffer(c["st"].cpu().numpy().tobytes(), dtype=abi.STATS_DTYPE)
+                  for c in cells]
+    ticks_local = int(sum(int(st["ticks"].sum()) for st in cell_stats))
+    unfinished = int(sum(int((st["status"] != abi.REPLAY_FINISHED).sum()) for st in cell_stats))
 
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(cells) + 1)]
+           for _ in range(args.steps)]
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -315,7 +360,9 @@ def main():
         if world > 1:
             dist.barrier()
     elapsed = start.elapsed_time(stop) / 1e3
-    replay_s = sum(e[0].elapsed_time(e[1]) for e in evs) / 1e3 / args.steps
+    replay_s = sum(e[0].elapsed_time(e[-1]) for e in evs) / 1e3 / args.steps
+    cell_ms = [sum(e[k].elapsed_time(e[k + 1]) for e in evs) / args.steps
+               for k in range(len(cells))]
     red_dev = dev if backend == "nccl" else "cpu"
     elapsed = rdist.max_over_ranks(elapsed, red_dev)          # slowest rank's device time
     ticks_total = rdist.sum_over_ranks(float(ticks_local), red_dev)
@@ -331,21 +378,24 @@ def main():
         hout = [torch.empty(N, dtype=d, pin_memory=True) for d in
                 (torch.int32, torch.float64, torch.float64, torch.float64, torch.int32,
                  torch.uint8)]
-        h_st = torch.zeros(R * 256, dtype=torch.uint8, pin_memory=True)
+        h_st = [torch.zeros(R * 256, dtype=torch.uint8, pin_memory=True) for _ in cells]
         htr = abi.TraceSoA(R, 0, N, h_off.data_ptr(), h_arr.data_ptr(), h_pr.data_ptr(),
                            h_de.data_ptr(), h_tk.data_ptr(), None, h_ps.data_ptr(), None)
         hro_full = abi.ReqOut(*[x.data_ptr() for x in hout])
         hro_stats = abi.ReqOut(None, None, None, None, None, None)
-        h2d = 8 * (R + 1) + 8 * N + 4 * N + 4 * N + N + 8 * R
-        if policy == "rl":
-            h2d += 8 * abi.mlp_param_count(agent_for(m)[0])
-        d2h_stats = 256 * R
-        d2h_full = N * (4 + 8 + 8 + 8 + 4 + 1) + 256 * R
+        # per cell (one rs_replay_batch_host call each) the inputs go up again
+        h2d = len(cells) * (8 * (R + 1) + 8 * N + 4 * N + 4 * N + N + 8 * R)
+        for c in cells:
+            if c["policy"] == "rl":
+                h2d += 8 * abi.mlp_param_count(agent_for(m)[0])
+        d2h_stats = 256 * R * len(cells)
+        d2h_full = (N * (4 + 8 + 8 + 8 + 4 + 1) + 256 * R) * len(cells)
 
         def timed_e2e(hro):
             def e2e_step():
-                abi.check(lib, lib.rs_replay_batch_host(C.byref(cfg), C.byref(htr), C.byref(hro),
-                                                        h_st.data_ptr(), local))
+                for c, hs in zip(cells, h_st):
+                    abi.check(lib, lib.rs_replay_batch_host(C.byref(c["cfg"]), C.byref(htr),
+                                                            C.byref(hro), hs.data_ptr(), local))
             e2e_step()  # warm the arena
             if world > 1:
                 dist.barrier()
@@ -368,9 +418,10 @@ def main():
                "with_per_request_d2h": {"value": ticks_total * args.steps / t_full,
                                         "d2h_bytes_per_step": int(d2h_full),
                                         "ms_per_step": t_full * 1e3 / args.steps}}
-        h_stats = np.frombuffer(h_st.numpy().tobytes(), dtype=abi.STATS_DTYPE)
-        if not np.array_equal(h_stats["decision_hash"], stats["decision_hash"]):
-            raise RuntimeError("e2e path decisions differ from the device path")
+        for hs, st in zip(h_st, cell_stats):
+            h_stats = np.frombuffer(hs.numpy().tobytes(), dtype=abi.STATS_DTYPE)
+            if not np.array_equal(h_stats["decision_hash"], st["decision_hash"]):
+                raise RuntimeError("e2e path decisions differ from the device path")
 
     if rank != 0:
         if world > 1:
@@ -378,7 +429,7 @@ def main():
         return
 
     peak, peak_src = load_peaks()
-    alg_bytes = REPLAY_BYTES_PER_REQUEST * N + REPLAY_BYTES_PER_REPLAY * R
+    alg_bytes = (REPLAY_BYTES_PER_REQUEST * N + REPLAY_BYTES_PER_REPLAY * R) * len(cells)
     achieved = alg_bytes / replay_s / 1e9
     traffic = None
     prof = ROOT / "profiles" / f"ncu_replay_{args.config}.json"
@@ -390,21 +441,24 @@ def main():
                 traffic = pj.get("dram_bytes_per_launch")
         except (ValueError, OSError):
             traffic = None
+    rate_s = (f"{rates[0]:g}" if len(rates) == 1 else f"{rates[0]:g}..{rates[-1]:g} "
+              f"({len(rates)} rates)")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic: reference workload generator, seeds 1..{R * world} "
-                f"(rank r takes seeds r*{R}+1..(r+1)*{R})",
-        "config": {"workload": desc, "policy": policy, "instances": m,
-                   "requests_per_replay": n, "replays_per_gpu": R, "arrival_rate": rate,
+        "data": f"synthetic: reference workload generator, seeds 1..{R_seeds * world} "
+                f"(rank r takes seeds r*{R_seeds}+1..(r+1)*{R_seeds})",
+        "config": {"workload": desc, "policy": "+".join(pols), "instances": m,
+                   "requests_per_replay": n, "replays_per_gpu": R * len(cells),
+                   "arrival_rate": rate_s,
                    "predictor": "simulated, Table-1 accuracy",
                    "l2": f"inputs {(8 + 4 + 4 + 1) * N / 1e6:.0f} MB per GPU > 126 MB L2 "
                          "(no flush needed)",
                    "parallelism": f"replay shards x{world} (weak)",
                    "prewarm_s": PREWARM_S},
         "decisions_per_step": ticks_total, "unfinished_replays": unfinished,
-        "gpu_launches": 2 * args.steps * world,
+        "gpu_launches": 2 * len(cells) * args.steps * world,
         "kernel_ms": {"replay_batch": replay_s * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
@@ -414,20 +468,22 @@ def main():
         "clocks": clk.summary(),
         "trace_gen_s": t_gen,
     }
+    if len(cells) > 1:
+        line["per_policy"] = {c["policy"]: {"decisions": int(st["ticks"].sum()),
+                                            "kernel_ms": ms,
+                                            "decisions_per_s": int(st["ticks"].sum()) / ms * 1e3}
+                              for c, st, ms in zip(cells, cell_stats, cell_ms)}
     if e2e:
         line["e2e"] = e2e
     if world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
             sample = min(threads, 64)
-            cv, cticks, cwall = cpu_reference(args.config if args.config != "c5" else "c5",
-                                              sample, threads)
+            cv, cticks, cwall, what = cpu_reference(args.config, sample, threads)
             line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": min(threads, sample),
                                     "kind": "reference",
-                                    "sample": f"{sample} replays (seeds 1..{sample}) of the "
-                                              f"{args.config} workload on {min(threads, sample)} "
-                                              f"host threads, {cwall:.1f} s wall, "
-                                              f"{cticks} decisions"}
+                                    "sample": f"{what} on {min(threads, sample)} host threads, "
+                                              f"{cwall:.1f} s wall, {cticks} decisions"}
         except Exception as e:  # baseline is reported, never the target
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}

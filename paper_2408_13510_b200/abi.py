@@ -271,6 +271,15 @@ def load_library(path: str | os.PathLike | None = None) -> C.CDLL:
     p = Path(path) if path else LIB_PATH
     if not p.exists():
         raise RuntimeError(f"engine library missing: {p} (run __graft_entry__.build())")
+    if path is None:
+        try:  # a library older than its sources is almost always a mistake
+            from . import build as _build
+            stamp = p.parent / ".stamp"
+            if stamp.exists() and stamp.read_text() != _build._digest():
+                import warnings
+                warnings.warn(f"{p} is older than its sources (run __graft_entry__.build())")
+        except OSError:
+            pass
     lib = C.CDLL(str(p))
     _declare(lib)
     if path is None:

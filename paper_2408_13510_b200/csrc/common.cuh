@@ -194,6 +194,87 @@ __device__ __forceinline__ long long warp_sum_ll(long long v) {
   return v;
 }
 
+// A lane group: W consecutive lanes of a warp that run one replay.  W = 32
+// is the whole warp (every collective compiles to its full-mask form); for
+// small fleets (m <= W < 32) a warp runs 32/W replays side by side, each
+// group's collectives restricted to its own lanes (segmented shuffles,
+// masked votes and reductions).  Control flow is uniform within a group and
+// may diverge between the groups of a warp.
+template <int W>
+struct Lanes {
+  static_assert(W == 4 || W == 8 || W == 16 || W == 32, "lane group width");
+  int l;          // lane within the group, 0..W-1
+  int base;       // first warp lane of the group
+  unsigned mask;  // the group's lanes
+
+  __device__ __forceinline__ unsigned m() const { return W == kWarp ? kFull : mask; }
+  // group-local vote bits (bit k = group lane k)
+  __device__ __forceinline__ unsigned ballot(bool p) const {
+    return W == kWarp ? __ballot_sync(kFull, p) : (__ballot_sync(mask, p) >> base);
+  }
+  __device__ __forceinline__ bool any(bool p) const { return __any_sync(m(), p); }
+  template <class T>
+  __device__ __forceinline__ T shfl(T v, int src) const { return __shfl_sync(m(), v, src, W); }
+  template <class T>
+  __device__ __forceinline__ T shfl_up(T v, int d) const { return __shfl_up_sync(m(), v, d, W); }
+  template <class T>
+  __device__ __forceinline__ T shfl_xor(T v, int o) const { return __shfl_xor_sync(m(), v, o, W); }
+  __device__ __forceinline__ int sum(int v) const {
+    return (int)__reduce_add_sync(m(), (unsigned)v);
+  }
+  __device__ __forceinline__ int min(int v) const { return __reduce_min_sync(m(), v); }
+  __device__ __forceinline__ int max(int v) const { return __reduce_max_sync(m(), v); }
+  __device__ __forceinline__ unsigned long long min_u64(unsigned long long v) const {
+#pragma unroll
+    for (int o = W >> 1; o > 0; o >>= 1) {
+      const unsigned long long w = shfl_xor(v, o);
+      v = w < v ? w : v;
+    }
+    return v;
+  }
+  __device__ __forceinline__ unsigned long long max_u64(unsigned long long v) const {
+#pragma unroll
+    for (int o = W >> 1; o > 0; o >>= 1) {
+      const unsigned long long w = shfl_xor(v, o);
+      v = w > v ? w : v;
+    }
+    return v;
+  }
+  __device__ __forceinline__ long long sum_ll(long long v) const {
+#pragma unroll
+    for (int o = W >> 1; o > 0; o >>= 1) v += shfl_xor(v, o);
+    return v;
+  }
+  __device__ __forceinline__ void sync() const { __syncwarp(m()); }
+  // group-local mask of the lanes below this one
+  __device__ __forceinline__ unsigned lt() const {
+    unsigned b;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(b));
+    return W == kWarp ? b : (b >> base);
+  }
+};
+
+// The calling thread's group (lane id laundered so it is computed once).
+template <int W>
+__device__ __forceinline__ Lanes<W> make_lanes() {
+  int t = threadIdx.x & (kWarp - 1);
+  asm volatile("" : "+r"(t));
+  Lanes<W> L;
+  L.l = t & (W - 1);
+  L.base = t & ~(W - 1);
+  L.mask = W == kWarp ? kFull : (((1u << (W & 31)) - 1u) << L.base);
+  return L;
+}
+
+// Whole-warp group for a known lane (the general kernel and predictor).
+__device__ __forceinline__ Lanes<kWarp> warp_lanes(int l) {
+  Lanes<kWarp> L;
+  L.l = l;
+  L.base = 0;
+  L.mask = kFull;
+  return L;
+}
+
 // Inclusive prefix sum across the warp.
 __device__ __forceinline__ int warp_incl_scan(int v, int l) {
 #pragma unroll
@@ -240,45 +321,71 @@ __device__ __forceinline__ unsigned long long hash_action(unsigned long long h, 
 }
 
 // ----------------------------------------------------- std::mt19937_64
-// Warp-cooperative block generation of 312 outputs into shared memory.
-// `s` holds the 312-word state.  Three dependency phases of the twist
-// (i < 156 reads only old words; 156 <= i < 311 reads new s[i-156]; i = 311
-// reads new s[0]), then tempering.
-__device__ inline void mt_twist_warp(unsigned long long* s, int l) {
-  auto tw = [](unsigned long long a, unsigned long long b) {
-    unsigned long long x = (a & 0xFFFFFFFF80000000ull) | (b & 0x7FFFFFFFull);
-    unsigned long long xa = x >> 1;
-    if (x & 1ull) xa ^= 0xB5026F5AA96619E9ull;
-    return xa;
-  };
-  unsigned long long nv[5];
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    int i = l + 32 * k;
-    if (i < 156) nv[k] = s[i + 156] ^ tw(s[i], s[i + 1]);
-  }
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    int i = l + 32 * k;
-    if (i < 156) s[i] = nv[k];
-  }
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    int i = 156 + l + 32 * k;
-    if (i < 311) nv[k] = s[i - 156] ^ tw(s[i], s[i + 1]);
-  }
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-    int i = 156 + l + 32 * k;
-    if (i < 311) s[i] = nv[k];
-  }
-  __syncwarp();
-  if (l == 0) s[311] = s[155] ^ tw(s[311], s[0]);
-  __syncwarp();
+// Group-cooperative block generation of the next 312 state words.  Three
+// dependency phases of the twist (i < 156 reads only old words; 156 <= i <
+// 311 reads new s[i-156]; i = 311 reads new s[0]).  A whole warp holds its
+// <= 5 new words per phase in registers; a narrower group walks each phase
+// in ascending W-word chunks (a chunk reads s[i+1] of the next, still old,
+// chunk before anything above it is written).
+__device__ __forceinline__ unsigned long long mt_tw(unsigned long long a, unsigned long long b) {
+  const unsigned long long x = (a & 0xFFFFFFFF80000000ull) | (b & 0x7FFFFFFFull);
+  unsigned long long xa = x >> 1;
+  if (x & 1ull) xa ^= 0xB5026F5AA96619E9ull;
+  return xa;
 }
+
+template <int W>
+__device__ inline void mt_twist(unsigned long long* s, const Lanes<W>& L) {
+  const int l = L.l;
+  if (W == kWarp) {
+    unsigned long long nv[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int i = l + 32 * k;
+      if (i < 156) nv[k] = s[i + 156] ^ mt_tw(s[i], s[i + 1]);
+    }
+    L.sync();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int i = l + 32 * k;
+      if (i < 156) s[i] = nv[k];
+    }
+    L.sync();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int i = 156 + l + 32 * k;
+      if (i < 311) nv[k] = s[i - 156] ^ mt_tw(s[i], s[i + 1]);
+    }
+    L.sync();
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      const int i = 156 + l + 32 * k;
+      if (i < 311) s[i] = nv[k];
+    }
+  } else {
+    for (int c = 0; c < 156; c += W) {
+      const int i = c + l;
+      unsigned long long v = 0;
+      if (i < 156) v = s[i + 156] ^ mt_tw(s[i], s[i + 1]);
+      L.sync();
+      if (i < 156) s[i] = v;
+      L.sync();
+    }
+    for (int c = 156; c < 311; c += W) {
+      const int i = c + l;
+      unsigned long long v = 0;
+      if (i < 311) v = s[i - 156] ^ mt_tw(s[i], s[i + 1]);
+      L.sync();
+      if (i < 311) s[i] = v;
+      L.sync();
+    }
+  }
+  L.sync();
+  if (l == 0) s[311] = s[155] ^ mt_tw(s[311], s[0]);
+  L.sync();
+}
+
+__device__ inline void mt_twist_warp(unsigned long long* s, int l) { mt_twist(s, warp_lanes(l)); }
 
 __device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
   y ^= (y >> 29) & 0x5555555555555555ull;
@@ -288,14 +395,27 @@ __device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
   return y;
 }
 
-// Seeding (std::mt19937_64 constructor); serial recurrence, lane 0.
-__device__ inline void mt_seed_warp(unsigned long long* s, unsigned long long seed, int l) {
-  if (l == 0) {
+// twist + temper the next 312 outputs into ob[0..311]
+template <int W>
+__device__ inline void mt_refill(unsigned long long* s, unsigned long long* ob, const Lanes<W>& L) {
+  mt_twist(s, L);
+  for (int q = L.l; q < 312; q += W) ob[q] = mt_temper(s[q]);
+  L.sync();
+}
+
+// Seeding (std::mt19937_64 constructor); serial recurrence, group lane 0.
+template <int W>
+__device__ inline void mt_seed(unsigned long long* s, unsigned long long seed, const Lanes<W>& L) {
+  if (L.l == 0) {
     s[0] = seed;
     for (int i = 1; i < 312; ++i)
       s[i] = 6364136223846793005ull * (s[i - 1] ^ (s[i - 1] >> 62)) + (unsigned long long)i;
   }
-  __syncwarp();
+  L.sync();
+}
+
+__device__ inline void mt_seed_warp(unsigned long long* s, unsigned long long seed, int l) {
+  mt_seed(s, seed, warp_lanes(l));
 }
 
 // Rng::uniform (rng.hpp:29): (u64 >> 11) * 2^-53, exact.

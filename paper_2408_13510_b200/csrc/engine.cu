@@ -247,15 +247,16 @@ int env_int(const char* name, int dflt) {
 }
 
 template <typename K>
-rs_status launch_kernel(K kern, const rs::KParams& kp, int wpb, int block_smem, int num_replays,
-                        cudaStream_t st) {
+rs_status launch_kernel(K kern, const rs::KParams& kp, int wpb, int groups_per_warp,
+                        int block_smem, int num_replays, cudaStream_t st) {
   RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, block_smem));
   int dev = 0, sms = 0, per_sm = 0;
   RS_CUDA(cudaGetDevice(&dev));
   RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * rs::kWarp, block_smem));
   if (per_sm < 1) return fail(RS_ERR_UNSUPPORTED, "replay kernel does not fit on an SM");
-  const int want = (num_replays + wpb - 1) / wpb;
+  const int per_block = wpb * groups_per_warp;
+  const int want = (num_replays + per_block - 1) / per_block;
   const int grid = std::max(1, std::min(want, sms * per_sm));
   kern<<<grid, wpb * rs::kWarp, block_smem, st>>>(kp);
   RS_CUDA(cudaGetLastError());
@@ -270,30 +271,30 @@ using KernelFn = void (*)(rs::KParams);
 // parallel) instantiates that policy's general and fast replay kernels.
 namespace rs {
 using KernelFn = void (*)(KParams);
-KernelFn kernel_for_0(bool fast, int groups);
-KernelFn kernel_for_1(bool fast, int groups);
-KernelFn kernel_for_2(bool fast, int groups);
-KernelFn kernel_for_3(bool fast, int groups);
-KernelFn kernel_for_4(bool fast, int groups);
-KernelFn kernel_for_5(bool fast, int groups);
-KernelFn kernel_for_6(bool fast, int groups);
-KernelFn kernel_for_7(bool fast, int groups);
-KernelFn kernel_for_8(bool fast, int groups);
+KernelFn kernel_for_0(bool fast, int groups, int width);
+KernelFn kernel_for_1(bool fast, int groups, int width);
+KernelFn kernel_for_2(bool fast, int groups, int width);
+KernelFn kernel_for_3(bool fast, int groups, int width);
+KernelFn kernel_for_4(bool fast, int groups, int width);
+KernelFn kernel_for_5(bool fast, int groups, int width);
+KernelFn kernel_for_6(bool fast, int groups, int width);
+KernelFn kernel_for_7(bool fast, int groups, int width);
+KernelFn kernel_for_8(bool fast, int groups, int width);
 }  // namespace rs
 
 namespace {
 
-KernelFn kernel_for(int policy, bool fast, int groups) {
+KernelFn kernel_for(int policy, bool fast, int groups, int width) {
   switch (policy) {
-    case 0: return rs::kernel_for_0(fast, groups);
-    case 1: return rs::kernel_for_1(fast, groups);
-    case 2: return rs::kernel_for_2(fast, groups);
-    case 3: return rs::kernel_for_3(fast, groups);
-    case 4: return rs::kernel_for_4(fast, groups);
-    case 5: return rs::kernel_for_5(fast, groups);
-    case 6: return rs::kernel_for_6(fast, groups);
-    case 7: return rs::kernel_for_7(fast, groups);
-    case 8: return rs::kernel_for_8(fast, groups);
+    case 0: return rs::kernel_for_0(fast, groups, width);
+    case 1: return rs::kernel_for_1(fast, groups, width);
+    case 2: return rs::kernel_for_2(fast, groups, width);
+    case 3: return rs::kernel_for_3(fast, groups, width);
+    case 4: return rs::kernel_for_4(fast, groups, width);
+    case 5: return rs::kernel_for_5(fast, groups, width);
+    case 6: return rs::kernel_for_6(fast, groups, width);
+    case 7: return rs::kernel_for_7(fast, groups, width);
+    case 8: return rs::kernel_for_8(fast, groups, width);
   }
   return nullptr;
 }
@@ -636,43 +637,91 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     kp.smem_weights_bytes = 0;
     L.weights_bytes = 0;
   }
-  int best_wpb = 0, best_warps = 0;
+  // Launch plan for a lane-group width W (32/W replays per warp): warps
+  // per block maximising resident replays per SM (registers via the
+  // occupancy calculator, shared memory per replay slot; the RL weights are
+  // staged once per block, which favours wider blocks).
+  int sms = 0;
+  RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int wpb_env = env_int("RS_WARPS_PER_BLOCK", 0);
-  for (int wpb = 8; wpb >= 1; --wpb) {
-    if (wpb_env && wpb != wpb_env) continue;
-    const int bytes = L.weights_bytes + wpb * L.group_bytes;
-    if (bytes > smem_optin) continue;
-    const int blocks = std::min(32 / wpb, smem_sm / (bytes + 1024));
-    const int warps = blocks * wpb;
-    if (warps > best_warps) {
-      best_warps = warps;
-      best_wpb = wpb;
+  struct Plan {
+    int width = 0, wpb = 0, per_sm = 0, block_smem = 0;
+    long long capacity = 0;  // resident replays on the device
+    KernelFn kern = nullptr;
+  };
+  auto plan_for = [&](int width) -> Plan {
+    Plan pl;
+    pl.width = width;
+    pl.kern = kernel_for(cfg->policy, fast, groups, width);
+    if (!pl.kern) return pl;
+    const int gpw = rs::kWarp / width;
+    for (int wpb = 8; wpb >= 1; --wpb) {
+      if (wpb_env && wpb != wpb_env) continue;
+      const long long bytes = L.weights_bytes + (long long)wpb * gpw * L.group_bytes;
+      if (bytes > smem_optin) continue;
+      if (cudaFuncSetAttribute(pl.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+          cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      int per_sm = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.kern, wpb * rs::kWarp,
+                                                        (size_t)bytes) != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      per_sm = std::min(per_sm, (int)(smem_sm / (bytes + 1024)));
+      const long long cap = (long long)sms * per_sm * wpb * gpw;
+      if (cap > pl.capacity) {
+        pl.capacity = cap;
+        pl.wpb = wpb;
+        pl.per_sm = per_sm;
+        pl.block_smem = (int)bytes;
+      }
+    }
+    return pl;
+  };
+  // Lane-group width: the whole warp.  RS_GROUP_WIDTH = 4/8/16 packs 32/W
+  // replays per warp (m <= W, whole-prompt prefill): parity-exact, but
+  // measured 7-9x SLOWER on c4 (m = 4, 16k replays): the groups of a warp
+  // diverge every tick and their paths serialise, so a warp runs its
+  // replays back to back with none of the latency hiding separate warps get.
+  // Kept as an opt-in, tested configuration, not chosen automatically.
+  const int w_env = env_int("RS_GROUP_WIDTH", 0);
+  int width = rs::kWarp;
+  if (w_env) {
+    if (w_env != 4 && w_env != 8 && w_env != 16 && w_env != 32)
+      return fail(RS_ERR_INVALID_ARGUMENT, "RS_GROUP_WIDTH must be 4, 8, 16 or 32");
+    if (fast && groups == 1) {
+      int min_w = 4;
+      while (min_w < cfg->num_instances) min_w <<= 1;
+      width = std::max(w_env, min_w);
     }
   }
-  if (best_wpb == 0)
+  Plan pl = plan_for(width);
+  if (!pl.kern) return fail(RS_ERR_INVALID_ARGUMENT, "unknown policy");
+  if (pl.wpb == 0)
     return fail(RS_ERR_UNSUPPORTED, "per-replay shared-memory state exceeds one SM (" +
                                         std::to_string(L.weights_bytes + L.group_bytes) + " B)");
-  // When every replay fits in one wave, the kernel time is the slowest
-  // warp's: spread the replays evenly, ceil(R / #SMs) warps per SM (one
-  // block per SM when that is <= 8 warps), instead of packing some SMs.
-  {
-    int sms = 0;
-    RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // When every replay fits in one wave of whole-warp groups, the kernel time
+  // is the slowest warp's: spread the replays evenly, ceil(R / #SMs) warps
+  // per SM (one block per SM when that is <= 8 warps), instead of packing
+  // some SMs.
+  if (pl.width == rs::kWarp && !wpb_env) {
     const int need = (tr->num_replays + sms - 1) / std::max(1, sms);
-    if (!wpb_env && need <= best_warps && need <= 8) {
+    if (need <= pl.per_sm * pl.wpb && need <= 8) {
       for (int wpb = need; wpb >= 1; --wpb) {
         if (L.weights_bytes + wpb * L.group_bytes <= smem_optin) {
-          best_wpb = wpb;
+          pl.wpb = wpb;
+          pl.block_smem = L.weights_bytes + wpb * L.group_bytes;
           break;
         }
       }
     }
   }
-  const int block_smem = L.weights_bytes + best_wpb * L.group_bytes;
   RS_CUDA(cudaMemsetAsync(kp.work_counter, 0, sizeof(int), st));
-  KernelFn kern = kernel_for(cfg->policy, fast, groups);
-  if (!kern) return fail(RS_ERR_INVALID_ARGUMENT, "unknown policy");
-  rs_status s2 = launch_kernel(kern, kp, best_wpb, block_smem, tr->num_replays, st);
+  rs_status s2 = launch_kernel(pl.kern, kp, pl.wpb, rs::kWarp / pl.width, pl.block_smem,
+                               tr->num_replays, st);
   if (s2 != RS_OK) return s2;
   // nearest-rank percentiles (metrics.hpp:62-80), one CTA per replay
   if (inputs_done) RS_CUDA(cudaStreamWaitEvent(st, (cudaEvent_t)inputs_done, 0));
@@ -685,8 +734,6 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   sp.completion = kp.o_completion;
   sp.stats = stats;
   {
-    int sms = 0;
-    RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int grid = std::max(1, std::min(tr->num_replays, sms * 8));
     rs::percentile_kernel<<<grid, rs::kStatsThreads, 0, st>>>(sp);
     RS_CUDA(cudaGetLastError());

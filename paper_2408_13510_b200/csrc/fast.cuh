@@ -276,78 +276,119 @@ __device__ inline void lane_admit(const KParams& P, int gw, long long off, int i
   }
 }
 
-// Warp-cooperative rescan of instance i's running batch after a decode
+// Group-cooperative rescan of instance i's running batch after a decode
 // step: completions (emitted >= true) are stored and compacted away, then
 // every aggregate is recomputed exactly.  `owner` lane holds the instance.
+// A whole warp keeps its <= 4 entries per lane in registers; a narrower
+// group streams the batch in W-entry chunks, compacting as it goes (an
+// entry only ever moves down, onto a slot already read).
+template <int W>
 __device__ inline void warp_scan_instance(const KParams& P, int gw, long long off, int i,
-                                          int owner, Inst& I, int l) {
-  const int D = __shfl_sync(kFull, I.D, owner);
-  const int n = __shfl_sync(kFull, I.n, owner);
-  const double clock = __shfl_sync(kFull, I.clock, owner);
-  int rq[kMaxRunChunks], pr[kMaxRunChunks], dh[kMaxRunChunks], tr[kMaxRunChunks],
-      ky[kMaxRunChunks];
-  bool keep[kMaxRunChunks];
-  int ncomp = 0;
-#pragma unroll
-  for (int k = 0; k < kMaxRunChunks; ++k) {
-    const int j = k * kWarp + l;
-    keep[k] = false;
-    rq[k] = pr[k] = dh[k] = tr[k] = ky[k] = 0;
-    if (k * kWarp < n) {
-      bool done = false;
-      if (j < n) {
-        rq[k] = RQ(P, gw, i, j);
-        pr[k] = RP(P, gw, i, j);
-        dh[k] = RD(P, gw, i, j);
-        tr[k] = RT(P, gw, i, j);
-        ky[k] = RK(P, gw, i, j);
-        done = D + ky[k] >= tr[k];
-        if (done) P.o_completion[off + (rq[k] & kReqMask)] = clock;
-        keep[k] = !done;
-      }
-      ncomp += __popc(__ballot_sync(kFull, done));
-    }
-  }
+                                          int owner, Inst& I, const Lanes<W>& L) {
+  const int l = L.l;
+  const int D = L.shfl(I.D, owner);
+  const int n = L.shfl(I.n, owner);
+  const double clock = L.shfl(I.clock, owner);
   int res = 0, kv = 0, dl = 0, tl = 0, tok = 0, nge = 0, nxg = kBig, nxd = kBig;
-  int npos = 0;
+  int ncomp = 0;
+  auto account = [&](int pr, int dh, int tr, int ky) {
+    const int em = D + ky;
+    res += reserved_of(pr, dh, em);
+    kv += pr + em;
+    const int d = dh - em;
+    dl += d > 0 ? d : 0;
+    tl += tr - em;
+    tok += pr + em;
+    if (em >= dh) nge++;
+    else nxg = min(nxg, dh - ky);
+    nxd = min(nxd, tr - ky);
+  };
+  if (W == kWarp) {
+    int rq[kMaxRunChunks], pr[kMaxRunChunks], dh[kMaxRunChunks], tr[kMaxRunChunks],
+        ky[kMaxRunChunks];
+    bool keep[kMaxRunChunks];
 #pragma unroll
-  for (int k = 0; k < kMaxRunChunks; ++k) {
-    if (k * kWarp < n) {
-      if (ncomp) {
-        const unsigned km = __ballot_sync(kFull, keep[k]);
-        if (keep[k]) {
-          const int d = npos + __popc(km & lanemask_lt());
-          RQ(P, gw, i, d) = rq[k];
-          RP(P, gw, i, d) = pr[k];
-          RD(P, gw, i, d) = dh[k];
-          RT(P, gw, i, d) = tr[k];
-          RK(P, gw, i, d) = ky[k];
+    for (int k = 0; k < kMaxRunChunks; ++k) {
+      const int j = k * kWarp + l;
+      keep[k] = false;
+      rq[k] = pr[k] = dh[k] = tr[k] = ky[k] = 0;
+      if (k * kWarp < n) {
+        bool done = false;
+        if (j < n) {
+          rq[k] = RQ(P, gw, i, j);
+          pr[k] = RP(P, gw, i, j);
+          dh[k] = RD(P, gw, i, j);
+          tr[k] = RT(P, gw, i, j);
+          ky[k] = RK(P, gw, i, j);
+          done = D + ky[k] >= tr[k];
+          if (done) P.o_completion[off + (rq[k] & kReqMask)] = clock;
+          keep[k] = !done;
         }
-        npos += __popc(km);
-      }
-      if (keep[k]) {
-        const int em = D + ky[k];
-        res += reserved_of(pr[k], dh[k], em);
-        kv += pr[k] + em;
-        const int d = dh[k] - em;
-        dl += d > 0 ? d : 0;
-        tl += tr[k] - em;
-        tok += pr[k] + em;
-        if (em >= dh[k]) nge++;
-        else nxg = min(nxg, dh[k] - ky[k]);
-        nxd = min(nxd, tr[k] - ky[k]);
+        ncomp += __popc(L.ballot(done));
       }
     }
+    int npos = 0;
+#pragma unroll
+    for (int k = 0; k < kMaxRunChunks; ++k) {
+      if (k * kWarp < n) {
+        if (ncomp) {
+          const unsigned km = L.ballot(keep[k]);
+          if (keep[k]) {
+            const int d = npos + __popc(km & L.lt());
+            RQ(P, gw, i, d) = rq[k];
+            RP(P, gw, i, d) = pr[k];
+            RD(P, gw, i, d) = dh[k];
+            RT(P, gw, i, d) = tr[k];
+            RK(P, gw, i, d) = ky[k];
+          }
+          npos += __popc(km);
+        }
+        if (keep[k]) account(pr[k], dh[k], tr[k], ky[k]);
+      }
+    }
+  } else {
+    for (int c = 0; c < n; c += W) {
+      const int j = c + l;
+      int rq = 0, pr = 0, dh = 0, tr = 0, ky = 0;
+      bool keep = false;
+      if (j < n) {
+        rq = RQ(P, gw, i, j);
+        pr = RP(P, gw, i, j);
+        dh = RD(P, gw, i, j);
+        tr = RT(P, gw, i, j);
+        ky = RK(P, gw, i, j);
+        const bool done = D + ky >= tr;
+        if (done) P.o_completion[off + (rq & kReqMask)] = clock;
+        keep = !done;
+      }
+      const unsigned km = L.ballot(keep);
+      const int nv = c + W < n ? W : n - c;  // valid entries in this chunk
+      const int before = ncomp;
+      ncomp += nv - __popc(km);
+      L.sync();  // every lane has read its entry before any slot is rewritten
+      if (keep) {
+        const int d = c - before + __popc(km & L.lt());
+        if (d != j) {
+          RQ(P, gw, i, d) = rq;
+          RP(P, gw, i, d) = pr;
+          RD(P, gw, i, d) = dh;
+          RT(P, gw, i, d) = tr;
+          RK(P, gw, i, d) = ky;
+        }
+      }
+      if (keep) account(pr, dh, tr, ky);
+      L.sync();
+    }
   }
-  res = warp_sum(res);
-  kv = warp_sum(kv);
-  dl = warp_sum(dl);
-  tl = warp_sum(tl);
-  tok = warp_sum(tok);
-  nge = warp_sum(nge);
-  nxg = warp_min(nxg);
-  nxd = warp_min(nxd);
-  __syncwarp();
+  res = L.sum(res);
+  kv = L.sum(kv);
+  dl = L.sum(dl);
+  tl = L.sum(tl);
+  tok = L.sum(tok);
+  nge = L.sum(nge);
+  nxg = L.min(nxg);
+  nxd = L.min(nxd);
+  L.sync();
   if (l == owner) {
     I.n = n - ncomp;
     I.comps += ncomp;

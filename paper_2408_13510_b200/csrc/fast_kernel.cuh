@@ -33,39 +33,39 @@ __device__ __forceinline__ FeatI feat_of(const Inst& I) {
 
 // Lowest lane (< width) holding the minimal key among valid lanes; all valid
 // lanes lie below `width` (a power of two), so log2(width) butterfly rounds.
-__device__ __forceinline__ int argmin_narrow(unsigned long long key, bool valid, int width) {
+template <int W>
+__device__ __forceinline__ int argmin_narrow(const Lanes<W>& L, unsigned long long key, bool valid,
+                                             int width) {
   unsigned long long k = valid ? key : ~0ull;
   for (int o = width >> 1; o > 0; o >>= 1) {
-    const unsigned long long w = __shfl_xor_sync(kFull, k, o);
+    const unsigned long long w = L.shfl_xor(k, o);
     k = w < k ? w : k;
   }
-  const unsigned ok = __ballot_sync(kFull, valid && key == k);
+  const unsigned ok = L.ballot(valid && key == k);
   return ok ? __ffs(ok) - 1 : -1;
 }
 
-// decode-bucket counts (state edges) of instance i's running batch
-__device__ inline void warp_dbc(const KParams& P, int gw, int i, int owner, const Inst& I, int* dbc,
-                                int l) {
-  const int D = __shfl_sync(kFull, I.D, owner);
-  const int n = __shfl_sync(kFull, I.n, owner);
-  int cnt[RS_MAX_BUCKETS];
-#pragma unroll
-  for (int b = 0; b < RS_MAX_BUCKETS; ++b) cnt[b] = 0;
-  for (int j = l; j < n; j += kWarp) {
-    const int d = RD(P, gw, i, j) - (D + RK(P, gw, i, j));
-    cnt[bucket_of(P.state_edges, P.n_state_edges, d > 0 ? d : 0)]++;
-  }
-#pragma unroll
-  for (int b = 0; b < RS_MAX_BUCKETS; ++b) {
-    const int c = warp_sum(cnt[b]);
-    if (l == b) dbc[i * RS_MAX_BUCKETS + b] = c;
-  }
+// Lowest group lane whose key is minimal (maximal) among valid lanes; -1 if none.
+template <int W>
+__device__ __forceinline__ int grp_argmin_key(const Lanes<W>& L, unsigned long long key, bool valid) {
+  const unsigned long long k = valid ? key : ~0ull;
+  const unsigned long long mn = L.min_u64(k);
+  const unsigned ok = L.ballot(valid && k == mn);
+  return ok ? __ffs(ok) - 1 : -1;
+}
+template <int W>
+__device__ __forceinline__ int grp_argmax_key(const Lanes<W>& L, unsigned long long key, bool valid) {
+  const unsigned long long k = valid ? key : 0ull;
+  const unsigned long long mx = L.max_u64(k);
+  const unsigned ok = L.ballot(valid && k == mx);
+  return ok ? __ffs(ok) - 1 : -1;
 }
 
-template <int POL, int G>
+template <int POL, int G, int W>
 __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Replay& R,
                                   const Inst (&S)[G], bool has_head, const Rec& hr, int hb,
-                                  char* gbase, int l) {
+                                  char* gbase, const Lanes<W>& L) {
+  const int l = L.l;
   const int m = P.m;
   const int need = reserved_of(hr.prompt, hr.dhat, 0);
   if (POL == RS_POLICY_ROUND_ROBIN || POL == RS_POLICY_DEDICATED_SMALL_LARGE) {
@@ -80,8 +80,8 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
     bool ok = false;
 #pragma unroll
     for (int g = 0; g < G; ++g)
-      if (g * kWarp + l == t) ok = can_accept(P, feat_of(S[g]), need);
-    ok = __shfl_sync(kFull, ok, t & (kWarp - 1));
+      if (g * W + l == t) ok = can_accept(P, feat_of(S[g]), need);
+    ok = L.shfl(ok, t & (W - 1));
     if (!ok) return m;
     if (POL == RS_POLICY_ROUND_ROBIN) R.rr_next++;
     else if (m >= 2 && t >= 1) R.dsl_next++;
@@ -90,10 +90,10 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
     if (!has_head) return m;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const int i = g * kWarp + l;
+      const int i = g * W + l;
       const bool ok = i < m && (long long)P.kv_cap - feat_of(S[g]).res >= need;
-      const unsigned b = __ballot_sync(kFull, ok);
-      if (b) return g * kWarp + __ffs(b) - 1;
+      const unsigned b = L.ballot(ok);
+      if (b) return g * W + __ffs(b) - 1;
     }
     return m;
   } else if (POL == RS_POLICY_MAX_CAPACITY) {  // policies.hpp:150-170
@@ -102,20 +102,20 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
     int bi = -1;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const int i = g * kWarp + l;
+      const int i = g * W + l;
       const bool v = i < m;
       const unsigned long long k = v ? ordered_key(capacity_of(P, S[g].kv)) : 0ull;
-      const int a = warp_argmax_key(k, v);
+      const int a = grp_argmax_key(L, k, v);
       if (a >= 0) {
-        const unsigned long long ka = __shfl_sync(kFull, k, a);
-        if (bi < 0 || ka > bk) { bk = ka; bi = g * kWarp + a; }
+        const unsigned long long ka = L.shfl(k, a);
+        if (bi < 0 || ka > bk) { bk = ka; bi = g * W + a; }
       }
     }
     bool ok = false;
 #pragma unroll
     for (int g = 0; g < G; ++g)
-      if (g * kWarp + l == bi) ok = (long long)P.kv_cap - feat_of(S[g]).res >= need;
-    ok = __shfl_sync(kFull, ok, bi & (kWarp - 1));
+      if (g * W + l == bi) ok = (long long)P.kv_cap - feat_of(S[g]).res >= need;
+    ok = L.shfl(ok, bi & (W - 1));
     if (!ok) return m;
     R.mc_next = __dadd_rn(R.clock, 1.0);
     return bi;
@@ -125,7 +125,7 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
     const int per = 3 + nsb;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const int i = g * kWarp + l;
+      const int i = g * W + l;
       if (i < m) {
         const FeatI f = feat_of(S[g]);
         double* xi = x + i * per;
@@ -173,13 +173,13 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
       x[m * per + 1] = has_head ? __ddiv_rn((double)hr.prompt, 1024.0) : 0.0;
       x[m * per + 2] = has_head ? (double)hb : 0.0;
     }
-    __syncwarp();
+    L.sync();
     const int na = P.rl_dims[P.rl_layers];
     if (P.rl_eps > 0.0) {  // DqnAgent::act (dqn.hpp:92-99)
       unsigned long long* rng = reinterpret_cast<unsigned long long*>(gbase + P.off_rng);
-      const double u = u01(rng_draw(rng, R, l));
+      const double u = u01(rng_draw(rng, R, L));
       if (u < P.rl_eps) {
-        const double v = __dmul_rn(u01(rng_draw(rng, R, l)), (double)na);
+        const double v = __dmul_rn(u01(rng_draw(rng, R, L)), (double)na);
         const unsigned long long k = (unsigned long long)v;
         return (int)(k < (unsigned long long)na ? k : (unsigned long long)na - 1);
       }
@@ -189,11 +189,11 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
       const int h0d = xd + P.rl_dims[0], h1d = h0d + P.rl_maxw, lvd = h1d + P.rl_maxw;
       const int lmax = P.rl_dims[0] > P.rl_maxw ? P.rl_dims[0] : P.rl_maxw;
       return mlp_forward_list(P.rl_dims, P.rl_woff, P.rl_boff, P.rl_layers, xd, h0d, h1d, lvd,
-                              (lvd + lmax) * 2, l);
+                              (lvd + lmax) * 2, L);
     }
     double* h0 = x + M.dims[0];
     double* h1 = h0 + P.rl_maxw;
-    return mlp_forward_warp(M, x, h0, h1, nullptr, l);
+    return mlp_forward_warp(M, x, h0, h1, nullptr, L);
   } else {  // argmin policies
     if (!has_head) return m;
     if (POL == RS_POLICY_DECODE_BALANCER || POL == RS_POLICY_WORKLOAD_AWARE) {
@@ -202,14 +202,14 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
       bool any_ok = false;
 #pragma unroll
       for (int g = 0; g < G; ++g)
-        any_ok |= (g * kWarp + l < m) && can_accept(P, feat_of(S[g]), need);
-      if (!__any_sync(kFull, any_ok)) return m;
+        any_ok |= (g * W + l < m) && can_accept(P, feat_of(S[g]), need);
+      if (!L.any(any_ok)) return m;
     }
     unsigned long long bk = ~0ull;
     int bi = -1;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const int i = g * kWarp + l;
+      const int i = g * W + l;
       bool v = i < m;
       unsigned long long k = ~0ull;
       if (v) {
@@ -238,10 +238,10 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
           k = ordered_key(__dsub_rn(__dadd_rn(avail, pcost), __dmul_rn(P.eps_s, mix)));
         }
       }
-      const int a = G == 1 ? argmin_narrow(k, v, P.mwidth) : warp_argmin_key(k, v);
+      const int a = G == 1 ? argmin_narrow(L, k, v, P.mwidth) : grp_argmin_key(L, k, v);
       if (a >= 0) {
-        const unsigned long long ka = __shfl_sync(kFull, k, a);
-        if (bi < 0 || ka < bk) { bk = ka; bi = g * kWarp + a; }
+        const unsigned long long ka = L.shfl(k, a);
+        if (bi < 0 || ka < bk) { bk = ka; bi = g * W + a; }
       }
     }
     if (POL == RS_POLICY_JSQ || POL == RS_POLICY_MIN_MIN) return bi;
@@ -255,7 +255,10 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
 // predict_simulated predictor.hpp:98-110: one draw, a second for a miss in a
 // middle bucket).  The stream is policy independent, so drawing a window
 // ahead of injection is equivalent.  Written to the predicted-bucket output.
-__device__ inline void predict_window(const KParams& P, Replay& R, unsigned long long* pst, int l) {
+template <int W>
+__device__ inline void predict_window(const KParams& P, Replay& R, unsigned long long* pst,
+                                      const Lanes<W>& L) {
+  const int l = L.l;
   const int j = R.a_base + l;
   const bool v = j < R.n;
   const long long g = R.off + j;
@@ -273,16 +276,14 @@ __device__ inline void predict_window(const KParams& P, Replay& R, unsigned long
       acc = P.accuracy[P.task[g]];
     }
     unsigned long long* ob = pst + 312;
-    const int cnt = min(kWarp, R.n - R.a_base);
+    const int cnt = min(W, R.n - R.a_base);
     for (int k = 0; k < cnt; ++k) {
-      const int tbk = __shfl_sync(kFull, tb, k);
-      const double ak = __shfl_sync(kFull, acc, k);
+      const int tbk = L.shfl(tb, k);
+      const double ak = L.shfl(acc, k);
       int pk = 0;
       if (nb > 1) {
         if (R.pred_pos == 312) {
-          mt_twist_warp(pst, l);
-          for (int q = l; q < 312; q += kWarp) ob[q] = mt_temper(pst[q]);
-          __syncwarp();
+          mt_refill(pst, ob, L);
           R.pred_pos = 0;
         }
         const double u = u01(ob[R.pred_pos++]);
@@ -294,9 +295,7 @@ __device__ inline void predict_window(const KParams& P, Replay& R, unsigned long
           pk = nb - 2;
         } else {
           if (R.pred_pos == 312) {
-            mt_twist_warp(pst, l);
-            for (int q = l; q < 312; q += kWarp) ob[q] = mt_temper(pst[q]);
-            __syncwarp();
+            mt_refill(pst, ob, L);
             R.pred_pos = 0;
           }
           pk = u01(ob[R.pred_pos++]) < 0.5 ? tbk - 1 : tbk + 1;
@@ -306,23 +305,25 @@ __device__ inline void predict_window(const KParams& P, Replay& R, unsigned long
     }
   }
   if (v) P.o_pred[g] = (uint8_t)pred;
-  __syncwarp();
+  L.sync();
 }
 
+template <int W>
 __device__ __forceinline__ void load_window_fast(const KParams& P, Replay& R,
-                                                 unsigned long long* pst, int l) {
+                                                 unsigned long long* pst, const Lanes<W>& L) {
+  const int l = L.l;
   if (P.resident) {
     // streamed inputs: wait until the copy stream has landed this window
-    const int need = min(R.n, R.a_base + kWarp);
+    const int need = min(R.n, R.a_base + W);
     if (need > R.resident_seen) {
       // every lane acquires; the warp minimum is visible to all of them
-      int v = __reduce_min_sync(kFull, load_acquire(P.resident));
+      int v = L.min(load_acquire(P.resident));
       if (v < need) {
         const unsigned long long t0 = globaltimer_ns();
         while (v < need) {
           __nanosleep(256);
-          v = __reduce_min_sync(kFull, load_acquire(P.resident));
-          if (v < need && __any_sync(kFull, globaltimer_ns() - t0 > kStreamTimeoutNs)) {
+          v = L.min(load_acquire(P.resident));
+          if (v < need && L.any(globaltimer_ns() - t0 > kStreamTimeoutNs)) {
             R.status = RS_REPLAY_NOT_RUN;  // copy stream never delivered
             return;
           }
@@ -330,8 +331,8 @@ __device__ __forceinline__ void load_window_fast(const KParams& P, Replay& R,
       }
       R.resident_seen = v;
     }
-    const double prev_last = __shfl_sync(kFull, R.a_val, kWarp - 1);
-    load_arrival_window(P, R, l);
+    const double prev_last = L.shfl(R.a_val, W - 1);
+    load_arrival_window(P, R, L);
     // lazy validation of the window (the up-front pass cannot read inputs
     // that are still in flight): arrivals non-decreasing, token ranges, and
     // the 32-bit aggregate bound over the requests seen so far
@@ -345,30 +346,32 @@ __device__ __forceinline__ void load_window_fast(const KParams& P, Replay& R,
       bad = p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens;
       vm = p + (d > P.ub_max ? d : P.ub_max);
     }
-    const double up = __shfl_up_sync(kFull, R.a_val, 1);
+    const double up = L.shfl_up(R.a_val, 1);
     const double prev = l == 0 ? prev_last : up;
     if (v && j > 0 && R.a_val < prev) bad = true;
-    vm = warp_max(vm);
+    vm = L.max(vm);
     R.vmax = vm > R.vmax ? vm : R.vmax;
-    if (__any_sync(kFull, bad)) R.status = RS_REPLAY_INVALID_TRACE;
+    if (L.any(bad)) R.status = RS_REPLAY_INVALID_TRACE;
     else if ((long long)R.n * R.vmax > (1ll << 30)) R.status = RS_REPLAY_CAPACITY;
   } else {
-    load_arrival_window(P, R, l);
+    load_arrival_window(P, R, L);
   }
-  if (P.predict_inline) predict_window(P, R, pst, l);
+  if (P.predict_inline) predict_window(P, R, pst, L);
 }
 
 // ClusterSim::inject_arrivals (env.hpp:357-375): a cursor advance over the
 // register window of arrival times; the next window is predicted on load.
+template <int W>
 __device__ __forceinline__ void inject_fast(const KParams& P, Replay& R, unsigned long long* pst,
-                                            int l) {
+                                            const Lanes<W>& L) {
+  const int l = L.l;
   for (;;) {
     const int j = R.a_base + l;
     const bool ok = j >= R.cursor && j < R.n && R.a_val <= R.clock;
-    R.cursor += __popc(__ballot_sync(kFull, ok));
-    if (R.cursor == R.a_base + kWarp && R.cursor < R.n) {
-      R.a_base += kWarp;
-      load_window_fast(P, R, pst, l);
+    R.cursor += __popc(L.ballot(ok));
+    if (R.cursor == R.a_base + W && R.cursor < R.n) {
+      R.a_base += W;
+      load_window_fast(P, R, pst, L);
       if (R.status != RS_REPLAY_FINISHED) break;  // streamed window failed validation
       continue;
     }
@@ -377,9 +380,10 @@ __device__ __forceinline__ void inject_fast(const KParams& P, Replay& R, unsigne
 }
 
 // Returns true when the replay must be re-run instance-sequentially.
-template <int POL, int G>
+template <int POL, int G, int W>
 __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const MlpView& M, int r,
-                                bool seq, int l) {
+                                bool seq, const Lanes<W>& L) {
+  const int l = L.l;
   Replay R;
   R.off = P.offsets[r];
   R.n = (int)(P.offsets[r + 1] - R.off);
@@ -389,7 +393,7 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
 
   bool bad = false;
   int vmax = 0;
-  for (int j = l; j < R.n; j += kWarp) {
+  for (int j = l; j < R.n; j += W) {
     const long long g = off + j;
     P.o_instance[g] = -1;
     P.o_routed[g] = -1.0;
@@ -404,10 +408,10 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
     const int v = p + (d > P.ub_max ? d : P.ub_max);
     vmax = v > vmax ? v : vmax;
   }
-  bad = __any_sync(kFull, bad);
+  bad = L.any(bad);
   // 32-bit aggregate guard: every per-instance token sum is bounded by
   // N x max(prompt + max(decode, bucket bound)) (+ the running batch)
-  const bool too_big = (long long)R.n * warp_max(vmax) > (1ll << 30);
+  const bool too_big = (long long)R.n * L.max(vmax) > (1ll << 30);
   Inst S[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) inst_init(S[g]);
@@ -425,35 +429,35 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
   R.err_inst = -1;
   R.rng_pos = 312;
   R.a_base = 0;
-  R.h_base = -2 * kWarp;
+  R.h_base = -2 * W;
   R.h_prompt = R.h_true = R.h_bucket = 0;
   if (POL == RS_POLICY_RL && P.rl_eps > 0.0)
-    mt_seed_warp(reinterpret_cast<unsigned long long*>(gbase + P.off_rng),
-                 P.policy_seed ? P.policy_seed[r] : 0ull, l);
+    mt_seed(reinterpret_cast<unsigned long long*>(gbase + P.off_rng),
+            P.policy_seed ? P.policy_seed[r] : 0ull, L);
   unsigned long long* pst = reinterpret_cast<unsigned long long*>(gbase + P.off_pred);
   R.pred_pos = 312;
   R.a_val = 0.0;
   R.resident_seen = R.vmax = 0;
   if (P.predict_inline && P.predictor_mode == RS_PREDICTOR_SIMULATED)
-    mt_seed_warp(pst, P.predictor_seed[r], l);  // Rng(predictor_seed), env.hpp:173
-  __syncwarp();
-  load_window_fast(P, R, pst, l);
+    mt_seed(pst, P.predictor_seed[r], L);  // Rng(predictor_seed), env.hpp:173
+  L.sync();
+  load_window_fast(P, R, pst, L);
   // arrival time of the next request to inject (+inf when none is left)
   auto next_arrival = [&]() {
     const int k = R.cursor - R.a_base;
-    const double a = __shfl_sync(kFull, R.a_val, k & (kWarp - 1));
+    const double a = L.shfl(R.a_val, k & (W - 1));
     R.next_arr = R.cursor < R.n ? a : __longlong_as_double(0x7ff0000000000000ll);
   };
   R.hr_q = -1;
   R.hr_prompt = R.hr_true = R.hr_bucket = 0;
   if (bad) R.status = RS_REPLAY_INVALID_TRACE;
   else if (too_big) R.status = RS_REPLAY_CAPACITY;
-  else if (R.status == RS_REPLAY_FINISHED) inject_fast(P, R, pst, l);
+  else if (R.status == RS_REPLAY_FINISHED) inject_fast(P, R, pst, L);
   next_arrival();
 
   while (R.status == RS_REPLAY_FINISHED && R.completed != R.n && R.tick < P.max_ticks) {
     if (POL == RS_POLICY_MIN_MIN && queue_len<POL>(R) > 0) {
-      if (!minmin_pick(P, front, R, l)) { R.status = RS_REPLAY_CAPACITY; break; }
+      if (!minmin_pick(P, front, R, L)) { R.status = RS_REPLAY_CAPACITY; break; }
     }
     const bool has_head = queue_len<POL>(R) > 0;
     Rec hr;
@@ -467,7 +471,7 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
         hr.dhat = P.ub[hb];
         hr.emit = 0;
       } else {
-        hr = head_rec<POL>(P, front, R, &hb, l);
+        hr = head_rec<POL>(P, front, R, &hb, L);
         R.hr_q = hr.req;
         R.hr_prompt = hr.prompt;
         R.hr_true = hr.tru;
@@ -476,7 +480,7 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
     } else {
       hr.req = hr.prompt = hr.dhat = hr.tru = hr.emit = 0;
     }
-    const int action = decide_fast<POL, G>(P, gw, M, R, S, has_head, hr, hb, gbase, l);
+    const int action = decide_fast<POL, G, W>(P, gw, M, R, S, has_head, hr, hb, gbase, L);
     R.hash = hash_action(R.hash, action);
     if (action < 0 || action > m) { R.status = RS_REPLAY_BAD_ACTION; break; }
     const double t1 = __dadd_rn(R.clock, P.delta_t);
@@ -488,11 +492,11 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
         if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) {
           if (l == 0)
             for (int k = 0; k + 1 < R.nfront; ++k) front[k] = front[k + 1];
-          __syncwarp();
+          L.sync();
           R.nfront--;
         } else {
           R.qhead++;
-          if (POL == RS_POLICY_MIN_MIN) mm_skip_removed(P, R, l);
+          if (POL == RS_POLICY_MIN_MIN) mm_skip_removed(P, R, L);
         }
         if (l == 0) {
           P.o_routed[off + hr.req] = R.clock;
@@ -502,7 +506,7 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
         R.total_wait++;  // the enqueue (uniform; admissions are counted per lane)
 #pragma unroll
         for (int g = 0; g < G; ++g)
-          if (g * kWarp + l == action) {
+          if (g * W + l == action) {
             lane_enqueue(P, gw, off, action, S[g], hr, R.clock);
           }
       }
@@ -514,7 +518,7 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
     bool again = false;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const int i = g * kWarp + l;
+      const int i = g * W + l;
       act[g] = false;
       if (i < m && S[g].clock < t1) {
         if (S[g].n > 0 || S[g].w_cnt > 0) act[g] = true;
@@ -522,12 +526,12 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
       }
       again |= act[g];
     }
-    unsigned fl = __any_sync(kFull, again) ? 2u : 0u;
+    unsigned fl = L.any(again) ? 2u : 0u;
     while (fl & 2u) {
       if (seq) {  // only the lowest-index instance that still has work
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          const int i = g * kWarp + l;
+          const int i = g * W + l;
           act[g] = false;
           if (i < m && S[g].clock < t1) {
             if (S[g].n > 0 || S[g].w_cnt > 0) act[g] = true;
@@ -537,8 +541,8 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
         int g0 = G;
 #pragma unroll
         for (int g = G - 1; g >= 0; --g)
-          if (__ballot_sync(kFull, act[g])) g0 = g;
-        const unsigned lm = __ballot_sync(kFull, act[g0 < G ? g0 : 0]);
+          if (L.ballot(act[g])) g0 = g;
+        const unsigned lm = L.ballot(act[g0 < G ? g0 : 0]);
 #pragma unroll
         for (int g = 0; g < G; ++g) act[g] = act[g] && g == g0 && l == __ffs(lm) - 1;
       }
@@ -548,7 +552,7 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
       for (int g = 0; g < G; ++g) {
         if (!act[g]) continue;
         Inst& I = S[g];
-        const int i = g * kWarp + l;
+        const int i = g * W + l;
         if (I.n == 0 && I.w_cnt == 0) {  // emptied by last iteration's events
           I.clock = t1;
           act[g] = false;
@@ -605,11 +609,11 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
       for (int g = 0; g < G; ++g) {
         act[g] = act[g] && S[g].clock < t1;
         // sequential mode keeps going while ANY instance still has a step
-        again |= seq ? (g * kWarp + l < m && S[g].clock < t1 &&
+        again |= seq ? (g * W + l < m && S[g].clock < t1 &&
                         (S[g].n > 0 || S[g].w_cnt > 0))
                      : act[g];
       }
-      fl = (__any_sync(kFull, again) ? 2u : 0u) | (__any_sync(kFull, ev) ? 1u : 0u);
+      fl = (L.any(again) ? 2u : 0u) | (L.any(ev) ? 1u : 0u);
       if (!(fl & 1u)) continue;
       // ---- events (whole warp): errors, completion scans, preemption ----
       {
@@ -617,8 +621,8 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
 #pragma unroll
         for (int g = 0; g < G; ++g)
           if ((evg >> g) & 1u)
-            if (S[g].n == 0) err = min(err, g * kWarp + l);
-        err = warp_min(err);
+            if (S[g].n == 0) err = min(err, g * W + l);
+        err = L.min(err);
         if (err != kBig) {
           if (!seq) return true;  // exact stop point needs index order: re-run
           R.status = RS_REPLAY_NOT_ADMISSIBLE;
@@ -631,15 +635,15 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
         const bool mine = (evg >> g) & 1u;
         const bool sc = mine && (S[g].D >= S[g].next_done || S[g].D >= S[g].next_ge) &&
                         S[g].npf == 0 && S[g].el_n == S[g].n;
-        unsigned sm = __ballot_sync(kFull, sc);
+        unsigned sm = L.ballot(sc);
         while (sm) {
           const int owner = __ffs(sm) - 1;
           sm &= sm - 1;
-          warp_scan_instance(P, gw, off, g * kWarp + owner, owner, S[g], l);
+          warp_scan_instance(P, gw, off, g * W + owner, owner, S[g], L);
         }
         if (mine && S[g].kv > P.kv_cap && S[g].n > 1) {
           const int w0 = S[g].w_cnt + S[g].o_cnt;
-          lane_preempt(P, gw, off, g * kWarp + l, S[g]);
+          lane_preempt(P, gw, off, g * W + l, S[g]);
           wdelta += S[g].w_cnt + S[g].o_cnt - w0;
         }
       }
@@ -654,15 +658,15 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
       if (S[g].clock < t1 && S[g].n == 0 && S[g].w_cnt == 0) S[g].clock = t1;
     }
     // one reduction: completions (low 16 bits) + biased waiting deltas
-    if (__any_sync(kFull, (comps | wdelta) != 0)) {
+    if (L.any((comps | wdelta) != 0)) {
       const unsigned packed =
-          warp_sum((int)((unsigned)comps | ((unsigned)(wdelta + 1024) << 16)));
+          L.sum((int)((unsigned)comps | ((unsigned)(wdelta + 1024) << 16)));
       R.completed += (int)(packed & 0xffffu);
-      R.total_wait += (int)(packed >> 16) - kWarp * 1024;
+      R.total_wait += (int)(packed >> 16) - W * 1024;
     }
     R.clock = t1;
     if (R.clock >= R.next_arr) {  // inject_arrivals (env.hpp:357-375) only when due
-      inject_fast(P, R, pst, l);
+      inject_fast(P, R, pst, L);
       next_arrival();
     }
     R.tick++;
@@ -670,14 +674,14 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
     R.sum_w += R.total_wait;
   }
   if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
-  write_replay_stats(P, R, r, l);
+  write_replay_stats(P, R, r, L);
   return false;
 }
 
-template <int POL, int G>
+template <int POL, int G, int W>
 __global__ void __launch_bounds__(256) replay_fast_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) char smem[];
-  const int l = opaque_lane();
+  const Lanes<W> L = make_lanes<W>();
   MlpView M;
   M.layers = P.rl_layers;
   M.dims = P.rl_dims;
@@ -694,17 +698,18 @@ __global__ void __launch_bounds__(256) replay_fast_kernel(const __grid_constant_
       groups_off = P.smem_weights_bytes;
     }
   }
-  int gbyte = groups_off + (int)(threadIdx.x / kWarp) * P.smem_group_bytes;
+  // one shared-memory slot per lane group (32/W replays per warp)
+  int gbyte = groups_off + (int)(threadIdx.x / W) * P.smem_group_bytes;
   asm volatile("" : "+r"(gbyte));  // keep the group base in a register
   char* gbase = smem + gbyte;
   const int gw = gbyte >> 2;
   for (;;) {
     int r = 0;
-    if (l == 0) r = atomicAdd(P.work_counter, 1);
-    r = __shfl_sync(kFull, r, 0);
+    if (L.l == 0) r = atomicAdd(P.work_counter, 1);
+    r = L.shfl(r, 0);
     if (r >= P.num_replays) break;
-    if (run_replay_fast<POL, G>(P, gw, gbase, M, r, false, l))
-      run_replay_fast<POL, G>(P, gw, gbase, M, r, true, l);
+    if (run_replay_fast<POL, G, W>(P, gw, gbase, M, r, false, L))
+      run_replay_fast<POL, G, W>(P, gw, gbase, M, r, true, L);
   }
 }
 

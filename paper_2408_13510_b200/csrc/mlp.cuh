@@ -33,8 +33,10 @@ struct MlpView {
 // Forward of one state vector `x` (shared memory, dims[0] doubles) by one
 // warp.  h0/h1: shared scratch of max width.  Writes the final layer to
 // `q_out` (may be nullptr) and returns argmax_action (dqn.hpp:82-90).
+template <int W>
 __device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double* h0,
-                                       double* h1, double* q_out, int l) {
+                                       double* h1, double* q_out, const Lanes<W>& L) {
+  const int l = L.l;
   const double* cur = x;
   unsigned long long best_key = 0;
   int best_idx = 0x7fffffff;
@@ -45,8 +47,8 @@ __device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double
     const double* B = M.w + M.boff[layer];
     const bool last = (layer + 1 == M.layers);
     double* dst = (layer & 1) ? h1 : h0;
-    for (int ob = 0; ob < no; ob += 2 * kWarp) {
-      const int o0 = ob + l, o1 = ob + kWarp + l;
+    for (int ob = 0; ob < no; ob += 2 * W) {
+      const int o0 = ob + l, o1 = ob + W + l;
       const bool v0 = o0 < no, v1 = o1 < no;
       double a0 = v0 ? B[o0] : 0.0;
       double a1 = v1 ? B[o1] : 0.0;
@@ -80,12 +82,17 @@ __device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double
         }
       }
     }
-    __syncwarp();
+    L.sync();
     cur = dst;
   }
-  const unsigned long long gmax = warp_max_u64(have ? best_key : 0ull);
+  const unsigned long long gmax = L.max_u64(have ? best_key : 0ull);
   const int cand = (have && best_key == gmax) ? best_idx : 0x7fffffff;
-  return warp_min(cand);
+  return L.min(cand);
+}
+
+__device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double* h0,
+                                       double* h1, double* q_out, int l) {
+  return mlp_forward_warp(M, x, h0, h1, q_out, warp_lanes(l));
 }
 
 extern __shared__ __align__(16) double rs_smd[];
@@ -94,83 +101,6 @@ extern __shared__ __align__(16) double rs_smd[];
 constexpr int kMlpMaskWords = 4;
 constexpr int kMlpSmemMaxWidth = kMlpMaskWords * kWarp;
 
-// Same forward with weights staged in shared memory at double index 0 and
-// x / h0 / h1 at double indices xd / h0d / h1d: every access is an LDS.64
-// with 32-bit addressing, and only the nonzero inputs are visited, in
-// ascending index order (ballot bitmasks), so each output still accumulates
-// acc = b; acc += w*x over i = 0..ni-1 with the zero terms omitted exactly
-// as in mlp_forward_warp.
-__device__ inline int mlp_forward_smem(const int* dims, const int* woff, const int* boff, int layers,
-                                       int xd, int h0d, int h1d, int l) {
-  int cur = xd;
-  // nonzero masks of the current input vector (<= 32 * kMlpMaskWords entries)
-  unsigned nz[kMlpMaskWords];
-  const int n0 = dims[0];
-#pragma unroll
-  for (int c = 0; c < kMlpMaskWords; ++c) {
-    const int i = c * kWarp + l;
-    nz[c] = c * kWarp < n0 ? __ballot_sync(kFull, i < n0 && rs_smd[cur + i] != 0.0) : 0u;
-  }
-  unsigned long long best_key = 0;
-  int best_idx = 0x7fffffff;
-  bool have = false;
-  for (int layer = 0; layer < layers; ++layer) {
-    const int ni = dims[layer], no = dims[layer + 1];
-    const int wt = woff[layer], bs = boff[layer];
-    const bool last = layer + 1 == layers;
-    const int dst = (layer & 1) ? h1d : h0d;
-    unsigned nn[kMlpMaskWords];
-#pragma unroll
-    for (int c = 0; c < kMlpMaskWords; ++c) nn[c] = 0u;
-    for (int ob = 0; ob < no; ob += 2 * kWarp) {
-      const int o0 = ob + l, o1 = ob + kWarp + l;
-      const bool v0 = o0 < no, v1 = o1 < no;
-      double a0 = v0 ? rs_smd[bs + o0] : 0.0;
-      double a1 = v1 ? rs_smd[bs + o1] : 0.0;
-      const int c0 = v0 ? o0 : 0, c1 = v1 ? o1 : 0;
-#pragma unroll
-      for (int c = 0; c < kMlpMaskWords; ++c) {
-        if (c * kWarp >= ni) break;
-        for (unsigned msk = nz[c]; msk; msk &= msk - 1) {
-          const int i = c * kWarp + __ffs(msk) - 1;
-          const double xi = rs_smd[cur + i];
-          const int row = wt + i * no;
-          a0 = __dadd_rn(a0, __dmul_rn(rs_smd[row + c0], xi));
-          a1 = __dadd_rn(a1, __dmul_rn(rs_smd[row + c1], xi));
-        }
-      }
-      if (!last) {
-        const double r0 = a0 > 0.0 ? a0 : 0.0, r1 = a1 > 0.0 ? a1 : 0.0;
-        if (v0) rs_smd[dst + o0] = r0;
-        if (v1) rs_smd[dst + o1] = r1;
-        const unsigned b0 = __ballot_sync(kFull, v0 && r0 != 0.0);
-        const unsigned b1 = __ballot_sync(kFull, v1 && r1 != 0.0);
-#pragma unroll
-        for (int c = 0; c < kMlpMaskWords; ++c) {
-          if (c == ob / kWarp) nn[c] = b0;
-          if (c == ob / kWarp + 1) nn[c] = b1;
-        }
-      } else {
-        if (v0) {
-          const unsigned long long k = ordered_key(a0);
-          if (!have || k > best_key) { best_key = k; best_idx = o0; have = true; }
-        }
-        if (v1) {
-          const unsigned long long k = ordered_key(a1);
-          if (!have || k > best_key) { best_key = k; best_idx = o1; have = true; }
-        }
-      }
-    }
-    __syncwarp();
-    cur = dst;
-#pragma unroll
-    for (int c = 0; c < kMlpMaskWords; ++c) nz[c] = nn[c];
-  }
-  const unsigned long long gmax = warp_max_u64(have ? best_key : 0ull);
-  const int cand = (have && best_key == gmax) ? best_idx : 0x7fffffff;
-  return warp_min(cand);
-}
-
 // Forward with weights staged in shared memory (double index 0), x / h0 / h1
 // at double indices xd / h0d / h1d, and a per-warp list of the current
 // layer's nonzero inputs (value at lvd + k, W^T row offset at int index
@@ -178,11 +108,13 @@ __device__ inline int mlp_forward_smem(const int* dims, const int* woff, const i
 // counted loop (unrolled, loads prefetched) over the nonzero terms only:
 // each output still adds w*x for i = 0..ni-1 in order, zero terms omitted
 // exactly as in mlp_forward_warp.
+template <int W>
 __device__ inline int mlp_forward_list(const int* dims, const int* woff, const int* boff,
                                        int layers, int xd, int h0d, int h1d, int lvd, int lid,
-                                       int l) {
+                                       const Lanes<W>& L) {
   int* rs_smi = reinterpret_cast<int*>(rs_smd);
-  const unsigned lt = lanemask_lt();
+  const int l = L.l;
+  const unsigned lt = L.lt();
   int cur = xd;
   unsigned long long best_key = 0;
   int best_idx = 0x7fffffff;
@@ -192,11 +124,11 @@ __device__ inline int mlp_forward_list(const int* dims, const int* woff, const i
     const int wt = woff[layer], bs = boff[layer];
     // compact the nonzero inputs of `cur`
     int nnz = 0;
-    for (int c = 0; c < ni; c += kWarp) {
+    for (int c = 0; c < ni; c += W) {
       const int i = c + l;
       const double v = i < ni ? rs_smd[cur + i] : 0.0;
       const bool nz = v != 0.0;
-      const unsigned msk = __ballot_sync(kFull, nz);
+      const unsigned msk = L.ballot(nz);
       if (nz) {
         const int p = nnz + __popc(msk & lt);
         rs_smd[lvd + p] = v;
@@ -204,11 +136,11 @@ __device__ inline int mlp_forward_list(const int* dims, const int* woff, const i
       }
       nnz += __popc(msk);
     }
-    __syncwarp();
+    L.sync();
     const bool last = layer + 1 == layers;
     const int dst = (layer & 1) ? h1d : h0d;
-    for (int ob = 0; ob < no; ob += 2 * kWarp) {
-      const int o0 = ob + l, o1 = ob + kWarp + l;
+    for (int ob = 0; ob < no; ob += 2 * W) {
+      const int o0 = ob + l, o1 = ob + W + l;
       const bool v0 = o0 < no, v1 = o1 < no;
       double a0 = v0 ? rs_smd[bs + o0] : 0.0;
       double a1 = v1 ? rs_smd[bs + o1] : 0.0;
@@ -234,12 +166,12 @@ __device__ inline int mlp_forward_list(const int* dims, const int* woff, const i
         }
       }
     }
-    __syncwarp();
+    L.sync();
     cur = dst;
   }
-  const unsigned long long gmax = warp_max_u64(have ? best_key : 0ull);
+  const unsigned long long gmax = L.max_u64(have ? best_key : 0ull);
   const int cand = (have && best_key == gmax) ? best_idx : 0x7fffffff;
-  return warp_min(cand);
+  return L.min(cand);
 }
 
 // Element k of the reference flat vector -> its slot in the transposed layout.

@@ -50,11 +50,13 @@ __device__ __forceinline__ void store_inst(const Grp& G, int i, const InstHot& h
   __syncwarp();
 }
 
-// Head-window: request data of the range head (prompt, true decode, bucket).
-__device__ __forceinline__ void head_window(const KParams& P, Replay& R, int q, int l) {
-  if (q >= R.h_base && q < R.h_base + kWarp) return;
-  R.h_base = q & ~(kWarp - 1);
-  const int j = R.h_base + l;
+// Head-window: request data of the range head (prompt, true decode, bucket),
+// one request per group lane.
+template <int W>
+__device__ __forceinline__ void head_window(const KParams& P, Replay& R, int q, const Lanes<W>& L) {
+  if (q >= R.h_base && q < R.h_base + W) return;
+  R.h_base = q & ~(W - 1);
+  const int j = R.h_base + L.l;
   if (j < R.n) {
     R.h_prompt = P.prompt[R.off + j];
     R.h_true = P.decode[R.off + j];
@@ -62,43 +64,53 @@ __device__ __forceinline__ void head_window(const KParams& P, Replay& R, int q, 
   }
 }
 
+template <int W>
 __device__ __forceinline__ Rec load_req(const KParams& P, long long off, int req, int* bucket,
-                                       int l) {
+                                       const Lanes<W>& L) {
   int v[3] = {0, 0, 0};
-  if (l == 0) {
+  if (L.l == 0) {
     v[0] = P.prompt[off + req];
     v[1] = P.decode[off + req];
     v[2] = P.bucket[off + req];
   }
   Rec r;
   r.req = req;
-  r.prompt = __shfl_sync(kFull, v[0], 0);
-  r.tru = __shfl_sync(kFull, v[1], 0);
-  *bucket = __shfl_sync(kFull, v[2], 0);
+  r.prompt = L.shfl(v[0], 0);
+  r.tru = L.shfl(v[1], 0);
+  *bucket = L.shfl(v[2], 0);
   r.dhat = P.ub[*bucket];
   r.emit = 0;
   return r;
 }
 
-template <int POL>
+template <int POL, int W>
 __device__ __forceinline__ Rec head_rec(const KParams& P, int* front, Replay& R, int* bucket,
-                                       int l) {
-  if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) return load_req(P, R.off, front[0], bucket, l);
-  head_window(P, R, R.qhead, l);
+                                       const Lanes<W>& L) {
+  if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) return load_req(P, R.off, front[0], bucket, L);
+  head_window(P, R, R.qhead, L);
   const int s = R.qhead - R.h_base;
   Rec r;
   r.req = R.qhead;
-  r.prompt = __shfl_sync(kFull, R.h_prompt, s);
-  r.tru = __shfl_sync(kFull, R.h_true, s);
-  *bucket = __shfl_sync(kFull, R.h_bucket, s);
+  r.prompt = L.shfl(R.h_prompt, s);
+  r.tru = L.shfl(R.h_true, s);
+  *bucket = L.shfl(R.h_bucket, s);
   r.dhat = P.ub[*bucket];
   r.emit = 0;
   return r;
 }
+template <int POL>
+__device__ __forceinline__ Rec head_rec(const KParams& P, int* front, Replay& R, int* bucket, int l) {
+  return head_rec<POL>(P, front, R, bucket, warp_lanes(l));
+}
 
-__device__ __forceinline__ void load_arrival_window(const KParams& P, Replay& R, int l) {
-  const int j = R.a_base + l;
+// arrival window: one arrival time per group lane
+template <int W>
+__device__ __forceinline__ void load_arrival_window(const KParams& P, Replay& R, const Lanes<W>& L) {
+  const int j = R.a_base + L.l;
   R.a_val = j < R.n ? P.arrival[R.off + j] : __longlong_as_double(0x7ff0000000000000ll);
+}
+__device__ __forceinline__ void load_arrival_window(const KParams& P, Replay& R, int l) {
+  load_arrival_window(P, R, warp_lanes(l));
 }
 
 // ClusterSim::inject_arrivals (env.hpp:357-375): predictions were resolved
@@ -124,37 +136,47 @@ __device__ __forceinline__ int queue_len(const Replay& R) {
 }
 
 // Skip range entries that min_min moved to the front list.
-__device__ __forceinline__ void mm_skip_removed(const KParams& P, Replay& R, int l) {
+template <int W>
+__device__ __forceinline__ void mm_skip_removed(const KParams& P, Replay& R, const Lanes<W>& L) {
   while (R.qhead < R.cursor && R.n_removed > 0) {
     int rem = 0;
-    if (l == 0) rem = P.mm_removed[R.off + R.qhead];
-    rem = __shfl_sync(kFull, rem, 0);
+    if (L.l == 0) rem = P.mm_removed[R.off + R.qhead];
+    rem = L.shfl(rem, 0);
     if (!rem) break;
     R.qhead++;
     R.n_removed--;
   }
 }
+__device__ __forceinline__ void mm_skip_removed(const KParams& P, Replay& R, int l) {
+  mm_skip_removed(P, R, warp_lanes(l));
+}
 
 // MinMinPolicy::pick_queue_index (policies.hpp:179-191) + move_to_front
 // (env.hpp:234-243).  Queue order = front list, then the range in index
 // order minus removed entries.  Returns false on front-list overflow.
-__device__ inline bool minmin_pick(const KParams& P, int* front, Replay& R, int l) {
+template <int W>
+__device__ inline bool minmin_pick(const KParams& P, int* front, Replay& R, const Lanes<W>& L) {
+  const int l = L.l;
   unsigned long long fk = ~0ull;
   int fpos = 0x7fffffff;
-  if (R.nfront > 0) {
+  for (int c = 0; c < R.nfront; c += W) {  // front list (<= kMaxFront entries)
+    const int f = c + l;
     unsigned long long k = ~0ull;
-    if (l < R.nfront) {
-      const int req = front[l];
+    if (f < R.nfront) {
+      const int req = front[f];
       const double est = __dadd_rn(__dmul_rn(P.tpp, (double)P.prompt[R.off + req]),
                                    __dmul_rn(P.dtb, (double)P.ub[P.bucket[R.off + req]]));
       k = ordered_key(est);
     }
-    fk = warp_min_u64(k);
-    fpos = warp_min((l < R.nfront && k == fk) ? l : 0x7fffffff);
+    const unsigned long long mk = L.min_u64(k);
+    if (mk < fk) {
+      fk = mk;
+      fpos = L.min((f < R.nfront && k == mk) ? f : 0x7fffffff);
+    }
   }
   unsigned long long rk = ~0ull;
   int ridx = -1;
-  for (int c = R.qhead; c < R.cursor; c += kWarp) {
+  for (int c = R.qhead; c < R.cursor; c += W) {
     const int j = c + l;
     unsigned long long k = ~0ull;
     if (j < R.cursor) {
@@ -165,21 +187,21 @@ __device__ inline bool minmin_pick(const KParams& P, int* front, Replay& R, int 
         k = ordered_key(est);
       }
     }
-    const unsigned long long mk = warp_min_u64(k);
+    const unsigned long long mk = L.min_u64(k);
     if (mk < rk) {
       rk = mk;
-      ridx = warp_min((k == mk && j < R.cursor) ? j : 0x7fffffff);
+      ridx = L.min((k == mk && j < R.cursor) ? j : 0x7fffffff);
     }
   }
   if (R.nfront > 0 && fk <= rk) {  // front entry (earlier queue positions win ties)
     if (fpos == 0) return true;
     const int v = front[fpos];
-    __syncwarp();
+    L.sync();
     if (l == 0) {
       for (int k = fpos; k > 0; --k) front[k] = front[k - 1];
       front[0] = v;
     }
-    __syncwarp();
+    L.sync();
     return true;
   }
   if (ridx < 0) return true;
@@ -190,25 +212,28 @@ __device__ inline bool minmin_pick(const KParams& P, int* front, Replay& R, int 
     for (int k = R.nfront; k > 0; --k) front[k] = front[k - 1];
     front[0] = ridx;
   }
-  __syncwarp();
+  L.sync();
   R.nfront++;
   R.n_removed++;
-  mm_skip_removed(P, R, l);
+  mm_skip_removed(P, R, L);
   return true;
+}
+__device__ inline bool minmin_pick(const KParams& P, int* front, Replay& R, int l) {
+  return minmin_pick(P, front, R, warp_lanes(l));
 }
 
 // ε-greedy stream (DqnAgent::act, dqn.hpp:92-99) in shared memory.
+template <int W>
 __device__ __forceinline__ unsigned long long rng_draw(unsigned long long* rngbuf, Replay& R,
-                                                       int l) {
-  unsigned long long* st = rngbuf;
-  unsigned long long* ob = rngbuf + 312;
+                                                       const Lanes<W>& L) {
   if (R.rng_pos == 312) {
-    mt_twist_warp(st, l);
-    for (int k = l; k < 312; k += kWarp) ob[k] = mt_temper(st[k]);
-    __syncwarp();
+    mt_refill(rngbuf, rngbuf + 312, L);
     R.rng_pos = 0;
   }
-  return ob[R.rng_pos++];
+  return rngbuf[312 + R.rng_pos++];
+}
+__device__ __forceinline__ unsigned long long rng_draw(unsigned long long* rngbuf, Replay& R, int l) {
+  return rng_draw(rngbuf, R, warp_lanes(l));
 }
 
 // Router decision for one tick.  `has_head` / `hr` / `hb` describe the head.
@@ -342,11 +367,13 @@ __device__ inline int decide(const KParams& P, const Grp& G, const MlpView& M, R
 
 // Per-replay statistics (compute_metrics, metrics.hpp:84-162): fp64 sums are
 // sequential in pool-index order, bit-identical to the reference.
-__device__ inline void write_replay_stats(const KParams& P, const Replay& R, int r, int l) {
+template <int W>
+__device__ inline void write_replay_stats(const KParams& P, const Replay& R, int r, const Lanes<W>& L) {
+  const int l = L.l;
   double se = 0.0, st = 0.0, sb = 0.0, sw = 0.0;
   long long tbtc = 0, pre = 0, tok = 0;
   double fa = __longlong_as_double(0x7fefffffffffffffll), lc = 0.0;
-  for (int b0 = 0; b0 < R.n; b0 += kWarp) {
+  for (int b0 = 0; b0 < R.n; b0 += W) {
     const int j = b0 + l;
     const bool v = j < R.n;
     const long long g = R.off + j;
@@ -375,12 +402,12 @@ __device__ inline void write_replay_stats(const KParams& P, const Replay& R, int
       fa = arr < fa ? arr : fa;
       lc = comp > lc ? comp : lc;
     }
-    const unsigned cm = __ballot_sync(kFull, c), tm = __ballot_sync(kFull, htb),
-                   wm = __ballot_sync(kFull, hw);
+    const unsigned cm = L.ballot(c), tm = L.ballot(htb),
+                   wm = L.ballot(hw);
     // sequential sums in pool-index order (bit-identical to compute_metrics)
-    for (int k = 0; k < kWarp; ++k) {
-      const double ek = __shfl_sync(kFull, e, k), tk = __shfl_sync(kFull, t, k);
-      const double bk = __shfl_sync(kFull, tb, k), wk = __shfl_sync(kFull, w, k);
+    for (int k = 0; k < W; ++k) {
+      const double ek = L.shfl(e, k), tk = L.shfl(t, k);
+      const double bk = L.shfl(tb, k), wk = L.shfl(w, k);
       if ((cm >> k) & 1u) {
         se = __dadd_rn(se, ek);
         st = __dadd_rn(st, tk);
@@ -389,15 +416,15 @@ __device__ inline void write_replay_stats(const KParams& P, const Replay& R, int
       if ((wm >> k) & 1u) sw = __dadd_rn(sw, wk);
     }
   }
-  pre = warp_sum_ll(pre);
-  tok = warp_sum_ll(tok);
-  tbtc = warp_sum_ll(tbtc);
+  pre = L.sum_ll(pre);
+  tok = L.sum_ll(tok);
+  tbtc = L.sum_ll(tbtc);
   {
     unsigned long long a = (unsigned long long)__double_as_longlong(fa);
-    a = warp_min_u64(a);  // non-negative doubles order like their bits
+    a = L.min_u64(a);  // non-negative doubles order like their bits
     fa = __longlong_as_double((long long)a);
     unsigned long long b = (unsigned long long)__double_as_longlong(lc);
-    b = warp_max_u64(b);
+    b = L.max_u64(b);
     lc = __longlong_as_double((long long)b);
   }
   if (l == 0) {
@@ -431,7 +458,11 @@ __device__ inline void write_replay_stats(const KParams& P, const Replay& R, int
     for (int k = 0; k < 4; ++k) s._pad[k] = 0;
     P.stats[r] = s;
   }
-  __syncwarp();
+  L.sync();
+}
+
+__device__ inline void write_replay_stats(const KParams& P, const Replay& R, int r, int l) {
+  write_replay_stats(P, R, r, warp_lanes(l));
 }
 
 template <int POL>

@@ -18,17 +18,23 @@ pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
-@pytest.fixture(params=["fast", "general", "streamed"], autouse=True)
+@pytest.fixture(params=["fast", "general", "streamed", "packed"], autouse=True)
 def kernel_path(request, monkeypatch):
     """Every parity test runs on both replay kernels: the lane-per-instance
     fast kernel (whole-prompt prefill) and the general warp-per-instance one;
     "streamed" forces rs_replay_batch_host's chunked input copies overlapping
-    the fast kernel (taken whenever the replays have equal lengths)."""
+    the fast kernel (taken whenever the replays have equal lengths);
+    "packed" forces the narrowest lane group the fleet allows (32/W replays
+    per warp, W = max(4, next power of two >= m))."""
     if request.param == "general":
         monkeypatch.setenv("RS_FORCE_GENERAL", "1")
     else:
         monkeypatch.delenv("RS_FORCE_GENERAL", raising=False)
     monkeypatch.setenv("RS_STREAM_INPUTS", "1" if request.param == "streamed" else "0")
+    if request.param == "packed":
+        monkeypatch.setenv("RS_GROUP_WIDTH", "4")
+    else:
+        monkeypatch.delenv("RS_GROUP_WIDTH", raising=False)
     return request.param
 
 
@@ -266,3 +272,4 @@ def test_streamed_inputs_validate_per_window(gpu, kernel_path):
     assert O.compare(got[0], O.ora_run(cfg, traces[0], ps[0])) == []
     assert got[1].stats["status"][0] == abi.REPLAY_INVALID_TRACE
     assert got[2].stats["status"][0] == abi.REPLAY_INVALID_TRACE
+
