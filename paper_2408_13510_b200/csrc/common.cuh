@@ -395,14 +395,6 @@ __device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
   return y;
 }
 
-// twist + temper the next 312 outputs into ob[0..311]
-template <int W>
-__device__ inline void mt_refill(unsigned long long* s, unsigned long long* ob, const Lanes<W>& L) {
-  mt_twist(s, L);
-  for (int q = L.l; q < 312; q += W) ob[q] = mt_temper(s[q]);
-  L.sync();
-}
-
 // Seeding (std::mt19937_64 constructor); serial recurrence, group lane 0.
 template <int W>
 __device__ inline void mt_seed(unsigned long long* s, unsigned long long seed, const Lanes<W>& L) {

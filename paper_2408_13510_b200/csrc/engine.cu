@@ -107,12 +107,12 @@ Layout make_layout(const rs_batch_cfg& c, int wcap, bool fast) {
                        lmax * sizeof(int), 16);
   }
   L.off_rng = (int)off;
-  if (rl && c.rl_epsilon > 0.0) off = align_up(off + 624 * sizeof(unsigned long long), 16);
+  if (rl && c.rl_epsilon > 0.0) off = align_up(off + 312 * sizeof(unsigned long long), 16);
   L.off_front = (int)off;
   if (c.policy == RS_POLICY_MIN_MIN) off = align_up(off + rs::kMaxFront * sizeof(int), 16);
   L.off_pred = (int)off;  // fused predictor's mt19937_64 state + outputs
   if (fast && (c.flags & RS_FLAG_PREDICT_INLINE) && c.predictor_mode == RS_PREDICTOR_SIMULATED)
-    off = align_up(off + 624 * sizeof(unsigned long long), 16);
+    off = align_up(off + 312 * sizeof(unsigned long long), 16);
   L.group_bytes = (int)align_up(off, 128);
   L.weights_bytes = 0;
   if (rl) {
@@ -478,7 +478,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   // several replays resident per SM
   const int m_inst = cfg->num_instances;
   const int wdef = m_inst <= 16 ? 64 : (m_inst <= 32 ? 32 : 16);
-  const int wcap = std::max(8, std::min(128, env_int("RS_WAIT_RING", wdef)));
+  int wcap = std::max(8, std::min(128, env_int("RS_WAIT_RING", wdef)));
   // whole-prompt prefill (no chunking, m <= 64) takes the lane-per-instance
   // kernel; chunked prefill and larger fleets take the general kernel
   const bool fast = rs_internal_fast_path(cfg);
@@ -486,6 +486,29 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     return fail(RS_ERR_INVALID_ARGUMENT, "streamed inputs need the lane-per-instance kernel");
   const int groups = m_inst <= 32 ? 1 : 2;
   Layout L = make_layout(*cfg, wcap, fast);
+  {
+    // Throughput regime (more replays than ~16 per SM, the register limit):
+    // resident replays per SM are bounded by shared memory, so shrink the
+    // waiting ring (longer queues spill to the global overflow list) until
+    // 16 replays fit per SM, or the ring is down to 8 slots.
+    int dev0 = 0, sms0 = 0;
+    RS_CUDA(cudaGetDevice(&dev0));
+    RS_CUDA(cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0));
+    const int target = std::min<long long>(16, ((long long)tr->num_replays + sms0 - 1) / sms0);
+    auto per_sm = [&](const Layout& Lx) {
+      int best = 0;
+      for (int wpb = 1; wpb <= 8; ++wpb) {
+        const long long bytes = (long long)Lx.weights_bytes + (long long)wpb * Lx.group_bytes;
+        const int blocks = std::min<long long>(32 / wpb, (228 * 1024) / (bytes + 1024));
+        best = std::max(best, blocks * wpb);
+      }
+      return std::min(best, 16);
+    };
+    while (fast && !getenv("RS_WAIT_RING") && wcap > 8 && per_sm(L) < target) {
+      wcap >>= 1;
+      L = make_layout(*cfg, wcap, fast);
+    }
+  }
   rs::KParams kp;
   std::memset(&kp, 0, sizeof(kp));
   const rs_profile& p = cfg->profile;
@@ -719,6 +742,12 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
       }
     }
   }
+  if (env_int("RS_DEBUG_PLAN", 0))
+    fprintf(stderr,
+            "rs plan: policy %d fast %d groups %d width %d wpb %d blocks/SM %d block_smem %d "
+            "group_bytes %d weights %d resident replays %lld\n",
+            cfg->policy, (int)fast, groups, pl.width, pl.wpb, pl.per_sm, pl.block_smem,
+            L.group_bytes, L.weights_bytes, pl.capacity);
   RS_CUDA(cudaMemsetAsync(kp.work_counter, 0, sizeof(int), st));
   rs_status s2 = launch_kernel(pl.kern, kp, pl.wpb, rs::kWarp / pl.width, pl.block_smem,
                                tr->num_replays, st);

@@ -275,7 +275,6 @@ __device__ inline void predict_window(const KParams& P, Replay& R, unsigned long
       tb = bucket_of(P.pred_edges, nb, P.decode[g]);
       acc = P.accuracy[P.task[g]];
     }
-    unsigned long long* ob = pst + 312;
     const int cnt = min(W, R.n - R.a_base);
     for (int k = 0; k < cnt; ++k) {
       const int tbk = L.shfl(tb, k);
@@ -283,10 +282,10 @@ __device__ inline void predict_window(const KParams& P, Replay& R, unsigned long
       int pk = 0;
       if (nb > 1) {
         if (R.pred_pos == 312) {
-          mt_refill(pst, ob, L);
+          mt_twist(pst, L);  // outputs are tempered as they are drawn
           R.pred_pos = 0;
         }
-        const double u = u01(ob[R.pred_pos++]);
+        const double u = u01(mt_temper(pst[R.pred_pos++]));
         if (u < ak) {
           pk = tbk;
         } else if (tbk == 0) {
@@ -295,10 +294,10 @@ __device__ inline void predict_window(const KParams& P, Replay& R, unsigned long
           pk = nb - 2;
         } else {
           if (R.pred_pos == 312) {
-            mt_refill(pst, ob, L);
+            mt_twist(pst, L);
             R.pred_pos = 0;
           }
-          pk = u01(ob[R.pred_pos++]) < 0.5 ? tbk - 1 : tbk + 1;
+          pk = u01(mt_temper(pst[R.pred_pos++])) < 0.5 ? tbk - 1 : tbk + 1;
         }
       }
       if (l == k) pred = pk;

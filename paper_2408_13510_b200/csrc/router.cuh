@@ -227,10 +227,10 @@ template <int W>
 __device__ __forceinline__ unsigned long long rng_draw(unsigned long long* rngbuf, Replay& R,
                                                        const Lanes<W>& L) {
   if (R.rng_pos == 312) {
-    mt_refill(rngbuf, rngbuf + 312, L);
+    mt_twist(rngbuf, L);  // outputs are tempered as they are drawn
     R.rng_pos = 0;
   }
-  return rngbuf[312 + R.rng_pos++];
+  return mt_temper(rngbuf[R.rng_pos++]);
 }
 __device__ __forceinline__ unsigned long long rng_draw(unsigned long long* rngbuf, Replay& R, int l) {
   return rng_draw(rngbuf, R, warp_lanes(l));
