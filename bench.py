@@ -41,7 +41,7 @@ METRIC = "routing decisions/sec over batched trace replays (whole box) at 1/2/4/
 UNIT = "decisions/s"
 REPLAY_BYTES_PER_REQUEST = 8 + 4 + 4 + 1 + (4 + 8 + 8 + 8 + 4)  # in: arrival, prompt, decode, bucket; out
 REPLAY_BYTES_PER_REPLAY = 8 + 256  # offsets + stats record
-PREWARM_S = 2.0
+PREWARM_S = float(os.environ.get("RS_BENCH_PREWARM_S", "2.0"))  # 0 under ncu (tools/profile.sh)
 
 CONFIGS = {
     # name: (requests, seeds per GPU, instances, rate(s), policy (or policies), weights, description)

@@ -168,6 +168,45 @@ typedef struct rs_batch_cfg {
  * out->predicted_bucket; rs_predict_buckets is then not needed.  Needs
  * trace->predictor_seed (simulated) or trace->given_bucket (given). */
 #define RS_FLAG_PREDICT_INLINE 1u
+/* ClusterConfig::record_trajectory (env.hpp:131, 305-319): set by
+ * rs_replay_trajectory, which also evaluates the Eq. 3 reward per tick and
+ * records TickRecords; rs_replay_batch rejects it. */
+#define RS_FLAG_RECORD_TRAJECTORY 2u
+
+/* ShapingMode, env.hpp:22-38 */
+typedef enum rs_shaping {
+  RS_SHAPING_NONE = 0,
+  RS_SHAPING_ADDITIVE = 1,
+  RS_SHAPING_GUIDED = 2
+} rs_shaping;
+
+/* RewardConfig (env.hpp:40-71) + episode_k, and the TickRecord trajectory
+ * (env.hpp:150-168) of every replay, device buffers.  Replay r's tick t
+ * (TickRecord::tick, 1-based) is record r*capacity + (t-1); the m-wide
+ * fields hold instance i of that record at (r*capacity + t-1)*m + i.  Ticks
+ * past `capacity` are simulated but not recorded (rs_replay_stats.ticks has
+ * the true count).  Any array may be NULL (not recorded); when both
+ * queue_penalty and reward are NULL the O(active) Eq. 3 scan is skipped. */
+typedef struct rs_trajectory {
+  int64_t capacity;           /* records per replay */
+  double r_w;                 /* RewardConfig::r_w = 60 */
+  double gamma;               /* RewardConfig::gamma = 0.99 */
+  double beta_d;              /* RewardConfig::beta_d = 0.5 */
+  int32_t shaping;            /* rs_shaping, default GUIDED */
+  int32_t episode_k;          /* ClusterConfig::episode_k (c_k = shaping_coefficient(k)) */
+  double* time_s;             /* TickRecord::time (router clock after the tick) */
+  int32_t* action;            /* TickRecord::action */
+  double* queue_penalty;      /* RewardBreakdown::queue_penalty (Eq. 3 scan) */
+  int32_t* completions;       /* RewardBreakdown::completions */
+  double* h;                  /* RewardBreakdown::h (heuristic_h, impact.hpp:94-103) */
+  double* shaping_term;       /* RewardBreakdown::shaping = c_k * h */
+  double* reward;             /* RewardBreakdown::total */
+  uint8_t* infeasible_route;  /* RewardBreakdown::infeasible_route */
+  int32_t* router_queue;      /* TickRecord::router_queue_len */
+  int32_t* tokens_emitted;    /* TickRecord::tokens_emitted */
+  int32_t* instance_running;  /* [.. x m] TickRecord::instance_running */
+  int32_t* instance_waiting;  /* [.. x m] TickRecord::instance_waiting */
+} rs_trajectory;
 
 /* Struct-of-arrays trace batch, CSR over replays.  Request i of replay r is
  * element offsets[r] + i.  Field meaning follows Request (request.hpp:42-69). */
@@ -268,6 +307,18 @@ rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* trace,
                           void* workspace, size_t workspace_bytes,
                           void* cuda_stream);
 
+/* rs_replay_batch with ClusterConfig::record_trajectory (cfg->flags must
+ * carry RS_FLAG_RECORD_TRAJECTORY): additionally evaluates, per tick, the
+ * reward of ClusterSim::step (env.hpp:257-303: Eq. 3 queue penalty over the
+ * arrived, uncompleted requests in pool-index order, completions, the
+ * shaping term c_k * heuristic_h of the routed head) and writes the
+ * TickRecords (env.hpp:305-319) into `traj` (device buffers).  Always runs
+ * the general (warp-per-replay) kernel. */
+rs_status rs_replay_trajectory(const rs_batch_cfg* cfg, const rs_trace_soa* trace,
+                               rs_req_out* out, rs_replay_stats* stats,
+                               const rs_trajectory* traj, void* workspace,
+                               size_t workspace_bytes, void* cuda_stream);
+
 /* Pinned host memory for the _host entry points (cudaHostAlloc). */
 void* rs_host_alloc(size_t bytes);
 void rs_host_free(void* p);
@@ -278,6 +329,13 @@ void rs_host_free(void* p);
 rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* trace,
                                rs_req_out* out, rs_replay_stats* stats,
                                int32_t device);
+
+/* rs_replay_trajectory with host buffers (trace, outputs and the
+ * trajectory arrays in `traj`), on `device`; the reference-facing form of
+ * ClusterSim::trajectory() (env.hpp:203) for a batch. */
+rs_status rs_replay_trajectory_host(const rs_batch_cfg* cfg, const rs_trace_soa* trace,
+                                    rs_req_out* out, rs_replay_stats* stats,
+                                    const rs_trajectory* traj, int32_t device);
 
 /* Standalone stage kernels for per-stage parity (host buffers in/out). */
 /* Mlp::forward over `batch` state vectors (mlp.hpp:54-68). */

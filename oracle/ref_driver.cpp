@@ -210,7 +210,7 @@ struct ReplayIO {
 };
 
 int run_one(const rs_batch_cfg& c, const ReplayIO& io, rs_replay_stats* st,
-            const DqnAgent* agent, bool record) {
+            const DqnAgent* agent, bool record, const rs_trajectory* traj = nullptr) {
   ArrivalTrace trace;
   trace.requests.resize(static_cast<std::size_t>(io.n));
   for (int64_t i = 0; i < io.n; ++i) {
@@ -223,6 +223,14 @@ int run_one(const rs_batch_cfg& c, const ReplayIO& io, rs_replay_stats* st,
   }
   ClusterConfig cc = to_cluster(c, io.predictor_seed);
   cc.record_trajectory = record;  // TickRecords feed the queue-length sums
+  if (traj) {  // RewardConfig + episode_k of the trajectory request
+    cc.reward.r_w = traj->r_w;
+    cc.reward.gamma = traj->gamma;
+    cc.reward.beta_d = traj->beta_d;
+    cc.reward.shaping = static_cast<ShapingMode>(traj->shaping);
+    cc.episode_k = traj->episode_k;
+    cc.record_trajectory = true;
+  }
   ClusterSim sim(cc, std::move(trace));
   std::unique_ptr<RoutingPolicy> pol;
   HardwareProfile prof = cc.profile;
@@ -302,6 +310,29 @@ int run_one(const rs_batch_cfg& c, const ReplayIO& io, rs_replay_stats* st,
   st->first_arrival_s = first_arrival;
   st->last_completion_s = last_completion;
   st->makespan_s = last_completion - first_arrival;
+  if (traj) {  // ClusterSim::trajectory() into the rs_trajectory arrays (record 0)
+    const auto& tv = sim.trajectory();
+    const int m = c.num_instances;
+    int64_t k = 0;
+    for (const auto& t : tv) {
+      if (k >= traj->capacity) break;
+      if (traj->time_s) traj->time_s[k] = t.time;
+      if (traj->action) traj->action[k] = t.action;
+      if (traj->queue_penalty) traj->queue_penalty[k] = t.reward.queue_penalty;
+      if (traj->completions) traj->completions[k] = t.reward.completions;
+      if (traj->h) traj->h[k] = t.reward.h;
+      if (traj->shaping_term) traj->shaping_term[k] = t.reward.shaping;
+      if (traj->reward) traj->reward[k] = t.reward.total;
+      if (traj->infeasible_route) traj->infeasible_route[k] = t.reward.infeasible_route ? 1 : 0;
+      if (traj->router_queue) traj->router_queue[k] = t.router_queue_len;
+      if (traj->tokens_emitted) traj->tokens_emitted[k] = t.tokens_emitted;
+      for (int i = 0; i < m; ++i) {
+        if (traj->instance_running) traj->instance_running[k * m + i] = t.instance_running[i];
+        if (traj->instance_waiting) traj->instance_waiting[k * m + i] = t.instance_waiting[i];
+      }
+      ++k;
+    }
+  }
   if (io.action_log) {
     int64_t k = std::min<int64_t>(io.action_cap, static_cast<int64_t>(log.size()));
     std::memcpy(io.action_log, log.data(), static_cast<std::size_t>(k) * sizeof(int32_t));
@@ -405,6 +436,27 @@ int ref_run_replay(const rs_batch_cfg* cfg, int64_t n, const double* arrival,
                 instance, routed, first, completion, preemptions, predicted,
                 action_log, action_cap};
     return run_one(*cfg, io, stats, agent.get(), true);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// One replay with record_trajectory on: TickRecords (env.hpp:305-319) into
+// `traj` (host arrays, replay-local: record t-1 for tick t).
+int ref_run_trajectory(const rs_batch_cfg* cfg, int64_t n, const double* arrival,
+                       const int32_t* prompt, const int32_t* decode, const uint8_t* task,
+                       uint64_t predictor_seed, uint64_t policy_seed, int32_t* instance,
+                       double* routed, double* first, double* completion,
+                       int32_t* preemptions, uint8_t* predicted, rs_replay_stats* stats,
+                       const rs_trajectory* traj) {
+  try {
+    if (!check_cfg(*cfg)) return -1;
+    std::unique_ptr<DqnAgent> agent;
+    if (cfg->policy == RS_POLICY_RL) agent = make_agent(*cfg);
+    ReplayIO io{n, arrival, prompt, decode, task, predictor_seed, policy_seed,
+                instance, routed, first, completion, preemptions, predicted, nullptr, 0};
+    return run_one(*cfg, io, stats, agent.get(), true, traj);
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;

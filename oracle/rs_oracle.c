@@ -291,8 +291,9 @@ static void admit_waiting(sim_t* s, inst_t* I) { /* instance.hpp:149-195 */
   }
 }
 
-/* Instance::step (instance.hpp:203-277); returns completions or -1. */
-static int inst_step(sim_t* s, inst_t* I) {
+/* Instance::step (instance.hpp:203-277); returns completions or -1 and adds
+ * IterationOutcome::tokens_emitted to *tokens. */
+static int inst_step(sim_t* s, inst_t* I, int* tokens) {
   const rs_batch_cfg* c = s->c;
   const rs_profile* p = &c->profile;
   admit_waiting(s, I);
@@ -329,6 +330,7 @@ static int inst_step(sim_t* s, inst_t* I) {
     for (int i = 0; i < I->n_run; ++i) emit[n_emit++] = i;
   }
   I->clock += elapsed;
+  *tokens += n_emit;
   for (int k = 0; k < n_emit; ++k) {
     uint32_t r = I->run[emit[k]].req;
     s->emitted[r] += 1;
@@ -555,14 +557,70 @@ static int64_t heavy_decode_cutoff(const rs_profile* p, const rs_thresholds* t) 
   return c;
 }
 
+/* ------------------------------------------------------------- reward */
+
+/* mixing_for (impact.hpp:51-77) against InstanceLoad::token_sum (39-43). */
+static double mixing_for(const rs_impact* im, int64_t p, int64_t d, int64_t token_sum) {
+  double pi = (double)p;
+  double lead = im->prompt_exponent == 2 ? pi * pi : pi;
+  double t_p = im->grad1 * (lead + (double)token_sum);
+  double r_p = t_p <= im->epsilon_s ? 1.0 : 1.0 - t_p / im->epsilon_s;
+  double r_d = -im->grad2 * (double)(token_sum + p + d);
+  return im->alpha * r_p + (1.0 - im->alpha) * r_d;
+}
+
+/* heuristic_h (impact.hpp:94-103) over instance_loads() (env.hpp:341-354). */
+static double heuristic_h(const sim_t* s, int64_t p, int64_t d, int action) {
+  int m = s->c->num_instances;
+  double best = 0.0, chosen = 0.0;
+  for (int i = 0; i < m; ++i) {
+    const inst_t* I = &s->inst[i];
+    int64_t ts = 0;
+    for (int k = 0; k < I->n_run; ++k) ts += (int64_t)s->prompt[I->run[k].req] + s->emitted[I->run[k].req];
+    for (int64_t k = 0; k < I->wait.size; ++k) {
+      uint32_t r = dq_at(&I->wait, k);
+      ts += (int64_t)s->prompt[r] + s->emitted[r];
+    }
+    double sc = mixing_for(&s->c->impact, p, d, ts);
+    if (i == 0 || best < sc) best = sc; /* std::max(best, sc) */
+    if (i == action) chosen = sc;
+  }
+  return chosen - best;
+}
+
+/* Eq. 3 queue penalty: the reward scan of ClusterSim::step (env.hpp:289-298). */
+static double queue_penalty(const sim_t* s) {
+  const rs_profile* p = &s->c->profile;
+  double qp = 0.0;
+  for (int64_t i = 0; i < s->n; ++i) {
+    if (s->arrival[i] > s->clock || s->completion[i] >= 0.0) continue;
+    double d_hat = (double)dec_est(s, (uint32_t)i);
+    /* estimate_request_time, latency.hpp:87-92 */
+    double t_hat = p->prompt_time_per_token * (double)s->prompt[i] + p->decode_time_base * d_hat;
+    double f = (double)s->emitted[i] / d_hat;
+    qp += (1.0 / t_hat) * (1.0 - f);
+  }
+  return qp;
+}
+
+/* RewardConfig::shaping_coefficient (env.hpp:55-63). */
+static double shaping_coefficient(const rs_trajectory* t) {
+  switch (t->shaping) {
+    case RS_SHAPING_NONE: return 0.0;
+    case RS_SHAPING_ADDITIVE: return 1.0;
+    default: return t->gamma * exp(-t->beta_d * (double)t->episode_k);
+  }
+}
+
 /* -------------------------------------------------------------- replay */
 
-int ora_run_replay(const rs_batch_cfg* c, int64_t n, const double* arrival,
-                   const int32_t* prompt, const int32_t* decode, const uint8_t* task,
-                   const uint8_t* given, uint64_t predictor_seed, uint64_t policy_seed,
-                   int32_t* o_instance, double* o_routed, double* o_first,
-                   double* o_completion, int32_t* o_preempt, uint8_t* o_pred,
-                   rs_replay_stats* st, int32_t* action_log, int64_t action_cap) {
+static int run_impl(const rs_batch_cfg* c, int64_t n, const double* arrival,
+                    const int32_t* prompt, const int32_t* decode, const uint8_t* task,
+                    const uint8_t* given, uint64_t predictor_seed, uint64_t policy_seed,
+                    int32_t* o_instance, double* o_routed, double* o_first,
+                    double* o_completion, int32_t* o_preempt, uint8_t* o_pred,
+                    rs_replay_stats* st, int32_t* action_log, int64_t action_cap,
+                    const rs_trajectory* traj) {
   if (c->num_instances < 1 || c->max_batch_size < 1 || c->kv_capacity_tokens < 1) return -1;
   if (c->policy < 0 || c->policy >= RS_POLICY_COUNT) return -1;
   int m = c->num_instances;
@@ -629,11 +687,15 @@ int ora_run_replay(const rs_batch_cfg* c, int64_t n, const double* arrival,
     /* ClusterSim::step, env.hpp:251-322 */
     if (action < 0 || action > m) { status = RS_REPLAY_BAD_ACTION; break; }
     double t1 = S.clock + c->delta_t;
+    double bd_h = 0.0;
+    int bd_infeasible = 0;
     if (action < m && S.rq.size > 0) {
       uint32_t h = dq_at(&S.rq, 0);
       if ((int64_t)prompt[h] + decode[h] > c->kv_capacity_tokens) {
         S.infeasible++;
+        bd_infeasible = 1;
       } else {
+        if (traj) bd_h = heuristic_h(&S, prompt[h], dec_est(&S, h), action);
         S.rq.head = (S.rq.head + 1) % S.rq.cap;
         S.rq.size--;
         S.routed[h] = S.clock;
@@ -643,11 +705,11 @@ int ora_run_replay(const rs_batch_cfg* c, int64_t n, const double* arrival,
         dq_push_back(&I->wait, h);
       }
     }
-    int completions = 0;
+    int completions = 0, tokens = 0;
     for (int i = 0; i < m && !S.error; ++i) { /* run_until, instance.hpp:303-310 */
       inst_t* I = &S.inst[i];
       while (I->clock < t1 && (I->n_run > 0 || I->wait.size > 0)) {
-        int d = inst_step(&S, I);
+        int d = inst_step(&S, I, &tokens);
         if (d < 0) { S.error = 1; S.error_instance = i; break; }
         completions += d;
       }
@@ -660,6 +722,25 @@ int ora_run_replay(const rs_batch_cfg* c, int64_t n, const double* arrival,
     S.tick++;
     sum_q += S.rq.size;
     for (int i = 0; i < m; ++i) sum_w += S.inst[i].wait.size;
+    if (traj && S.tick <= traj->capacity) { /* TickRecord, env.hpp:300-319 */
+      int64_t k = S.tick - 1;
+      double qp = queue_penalty(&S);
+      double shaping = shaping_coefficient(traj) * bd_h;
+      if (traj->time_s) traj->time_s[k] = S.clock;
+      if (traj->action) traj->action[k] = action;
+      if (traj->queue_penalty) traj->queue_penalty[k] = qp;
+      if (traj->completions) traj->completions[k] = completions;
+      if (traj->h) traj->h[k] = bd_h;
+      if (traj->shaping_term) traj->shaping_term[k] = shaping;
+      if (traj->reward) traj->reward[k] = -qp + traj->r_w * (double)completions + shaping;
+      if (traj->infeasible_route) traj->infeasible_route[k] = (uint8_t)bd_infeasible;
+      if (traj->router_queue) traj->router_queue[k] = (int32_t)S.rq.size;
+      if (traj->tokens_emitted) traj->tokens_emitted[k] = tokens;
+      for (int i = 0; i < m; ++i) {
+        if (traj->instance_running) traj->instance_running[k * m + i] = S.inst[i].n_run;
+        if (traj->instance_waiting) traj->instance_waiting[k * m + i] = (int32_t)S.inst[i].wait.size;
+      }
+    }
   }
   if (status == RS_REPLAY_FINISHED && S.completed != n) status = RS_REPLAY_MAX_TICKS;
 
@@ -752,6 +833,29 @@ int ora_run_replay(const rs_batch_cfg* c, int64_t n, const double* arrival,
   free(P);
   free(F);
   return 0;
+}
+
+int ora_run_replay(const rs_batch_cfg* c, int64_t n, const double* arrival,
+                   const int32_t* prompt, const int32_t* decode, const uint8_t* task,
+                   const uint8_t* given, uint64_t predictor_seed, uint64_t policy_seed,
+                   int32_t* o_instance, double* o_routed, double* o_first,
+                   double* o_completion, int32_t* o_preempt, uint8_t* o_pred,
+                   rs_replay_stats* st, int32_t* action_log, int64_t action_cap) {
+  return run_impl(c, n, arrival, prompt, decode, task, given, predictor_seed, policy_seed,
+                  o_instance, o_routed, o_first, o_completion, o_preempt, o_pred, st,
+                  action_log, action_cap, NULL);
+}
+
+int ora_run_trajectory(const rs_batch_cfg* c, int64_t n, const double* arrival,
+                       const int32_t* prompt, const int32_t* decode, const uint8_t* task,
+                       const uint8_t* given, uint64_t predictor_seed, uint64_t policy_seed,
+                       int32_t* o_instance, double* o_routed, double* o_first,
+                       double* o_completion, int32_t* o_preempt, uint8_t* o_pred,
+                       rs_replay_stats* st, const rs_trajectory* traj) {
+  if (!traj) return -1;
+  return run_impl(c, n, arrival, prompt, decode, task, given, predictor_seed, policy_seed,
+                  o_instance, o_routed, o_first, o_completion, o_preempt, o_pred, st, NULL, 0,
+                  traj);
 }
 
 int ora_cmp_double(const void* a, const void* b) {

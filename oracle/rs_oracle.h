@@ -34,6 +34,18 @@ int ora_run_replay(const rs_batch_cfg* cfg, int64_t n, const double* arrival,
                    uint8_t* predicted, rs_replay_stats* stats,
                    int32_t* action_log, int64_t action_cap);
 
+/* ora_run_replay with record_trajectory: the Eq. 3 reward and TickRecords
+ * (env.hpp:257-319) of every tick into `traj` (host arrays; record t-1 for
+ * tick t, m-wide fields at (t-1)*m + i). */
+int ora_run_trajectory(const rs_batch_cfg* cfg, int64_t n, const double* arrival,
+                       const int32_t* prompt, const int32_t* decode,
+                       const uint8_t* task, const uint8_t* given_bucket,
+                       uint64_t predictor_seed, uint64_t policy_seed,
+                       int32_t* instance, double* routed, double* first,
+                       double* completion, int32_t* preemptions,
+                       uint8_t* predicted, rs_replay_stats* stats,
+                       const rs_trajectory* traj);
+
 /* inject_arrivals' prediction for every request in index order
  * (env.hpp:357-375). */
 int ora_predict_buckets(const rs_batch_cfg* cfg, int64_t n,

@@ -48,6 +48,8 @@ POLICY_NAMES = {v: k for k, v in POLICIES.items()}
 BATCHING = {"fcfs": 0, "bin_packing": 1, "least_work_left": 2}
 PRED_SIMULATED, PRED_EMPIRICAL, PRED_GIVEN = 0, 1, 2
 RS_FLAG_PREDICT_INLINE = 1  # rs_replay_batch draws predictions at injection
+RS_FLAG_RECORD_TRAJECTORY = 2  # ClusterConfig::record_trajectory (rs_replay_trajectory)
+SHAPING = {"none": 0, "additive": 1, "guided": 2}  # ShapingMode (env.hpp:22)
 
 # rs_replay_status
 REPLAY_FINISHED = 0
@@ -175,6 +177,39 @@ class ReplayStats(C.Structure):
 
 assert C.sizeof(ReplayStats) == 256, C.sizeof(ReplayStats)
 
+# TickRecord fields of rs_trajectory: (name, numpy dtype, m-wide)
+TRAJ_FIELDS = (("time_s", np.float64, False), ("action", np.int32, False),
+               ("queue_penalty", np.float64, False), ("completions", np.int32, False),
+               ("h", np.float64, False), ("shaping_term", np.float64, False),
+               ("reward", np.float64, False), ("infeasible_route", np.uint8, False),
+               ("router_queue", np.int32, False), ("tokens_emitted", np.int32, False),
+               ("instance_running", np.int32, True), ("instance_waiting", np.int32, True))
+
+
+class Trajectory(C.Structure):
+    """rs_trajectory: RewardConfig (env.hpp:40-71) + episode_k and the
+    TickRecord arrays (env.hpp:150-168)."""
+    _fields_ = [("capacity", C.c_int64), ("r_w", C.c_double), ("gamma", C.c_double),
+                ("beta_d", C.c_double), ("shaping", C.c_int32), ("episode_k", C.c_int32)] + [
+                   (name, C.c_void_p) for name, _, _ in TRAJ_FIELDS]
+
+
+def make_trajectory(capacity: int, replays: int, m: int, r_w: float = 60.0,
+                    gamma: float = 0.99, beta_d: float = 0.5, shaping: str = "guided",
+                    episode_k: int = 0, fields=None):
+    """A host rs_trajectory with numpy arrays for `fields` (default all):
+    returns (struct, {name: array shaped [replays, capacity(, m)]})."""
+    arrays = {}
+    t = Trajectory(int(capacity), r_w, gamma, beta_d, SHAPING[shaping], int(episode_k))
+    for name, dt, wide in TRAJ_FIELDS:
+        if fields is not None and name not in fields:
+            continue
+        shape = (replays, capacity, m) if wide else (replays, capacity)
+        a = np.zeros(shape, dt)
+        arrays[name] = a
+        setattr(t, name, a.ctypes.data)
+    return t, arrays
+
 # numpy view of rs_replay_stats for arrays of records
 _I64 = ("ticks", "routed", "infeasible", "completed")
 STATS_DTYPE = np.dtype(
@@ -293,6 +328,7 @@ EXPORTED_SYMBOLS = (
     "rs_replay_batch", "rs_replay_batch_host", "rs_mlp_forward_host",
     "rs_generate_mixture", "rs_generate_mixture_batch", "rs_mix_seed",
     "rs_heavy_decode_cutoff", "rs_host_alloc", "rs_host_free", "rs_mlp_random_init",
+    "rs_replay_trajectory", "rs_replay_trajectory_host",
 )
 
 
@@ -309,6 +345,10 @@ def _declare(lib: C.CDLL) -> None:
                                     C.c_void_p, C.c_size_t, C.c_void_p]
     lib.rs_replay_batch_host.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,
                                          C.c_int32]
+    lib.rs_replay_trajectory.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,
+                                         P(Trajectory), C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.rs_replay_trajectory_host.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,
+                                              P(Trajectory), C.c_int32]
     lib.rs_mlp_forward_host.argtypes = [P(BatchCfg), C.c_void_p, C.c_int32, C.c_void_p,
                                         C.c_void_p, C.c_int32]
     lib.rs_generate_mixture.argtypes = [P(Profile), P(Thresholds), C.c_void_p, C.c_uint64,

@@ -129,6 +129,12 @@ struct KParams {
   // replay are on the device; the copy stream raises it chunk by chunk while
   // the replay runs (nullptr = everything resident, validated up front)
   const int* resident;
+  // ClusterConfig::record_trajectory (general kernel only): per-tick reward
+  // (env.hpp:257-303) and TickRecords (env.hpp:305-319)
+  rs_trajectory traj;   // device arrays (by value); traj_on = 0: off
+  int traj_on;
+  double r_w, c_k;      // RewardConfig::r_w, shaping_coefficient(episode_k)
+  int traj_scan;        // evaluate the O(active) Eq. 3 queue-penalty scan
 };
 
 // acquire-load of the streamed-input watermark

@@ -436,8 +436,28 @@ rs_status rs_predict_buckets(const rs_batch_cfg* cfg, const rs_trace_soa* tr,
 rs_status rs_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_out* out,
                           rs_replay_stats* stats, void* workspace, size_t workspace_bytes,
                           void* stream) {
+  if (cfg && (cfg->flags & RS_FLAG_RECORD_TRAJECTORY))
+    return fail(RS_ERR_INVALID_ARGUMENT, "record_trajectory: use rs_replay_trajectory");
   return rs_internal_replay_batch(cfg, tr, out, stats, workspace, workspace_bytes, stream,
-                                  nullptr, nullptr);
+                                  nullptr, nullptr, nullptr);
+}
+
+rs_status rs_replay_trajectory(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_out* out,
+                               rs_replay_stats* stats, const rs_trajectory* traj,
+                               void* workspace, size_t workspace_bytes, void* stream) {
+  if (!cfg || !traj) return fail(RS_ERR_INVALID_ARGUMENT, "null config/trajectory");
+  if (traj->capacity < 0) return fail(RS_ERR_INVALID_ARGUMENT, "trajectory capacity < 0");
+  // RewardConfig::validate (env.hpp:46-52)
+  if (!(traj->r_w > 0.0)) return fail(RS_ERR_INVALID_ARGUMENT, "reward: r_w must be > 0");
+  if (!(traj->gamma >= 0.0 && traj->gamma < 1.0))
+    return fail(RS_ERR_INVALID_ARGUMENT, "reward: gamma outside [0, 1)");
+  if (!(traj->beta_d > 0.0)) return fail(RS_ERR_INVALID_ARGUMENT, "reward: beta_d must be > 0");
+  if (traj->shaping < RS_SHAPING_NONE || traj->shaping > RS_SHAPING_GUIDED)
+    return fail(RS_ERR_INVALID_ARGUMENT, "unknown shaping mode");
+  rs_batch_cfg c = *cfg;
+  c.flags |= RS_FLAG_RECORD_TRAJECTORY;
+  return rs_internal_replay_batch(&c, tr, out, stats, workspace, workspace_bytes, stream,
+                                  nullptr, nullptr, traj);
 }
 
 }  // extern "C"
@@ -455,7 +475,7 @@ bool rs_internal_fast_path(const rs_batch_cfg* cfg) {
 rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr,
                                    rs_req_out* out, rs_replay_stats* stats, void* workspace,
                                    size_t workspace_bytes, void* stream, const int* resident,
-                                   void* inputs_done) {
+                                   void* inputs_done, const rs_trajectory* traj) {
   rs_status s = validate(cfg);
   if (s != RS_OK) return s;
   if ((s = require_device()) != RS_OK) return s;
@@ -481,7 +501,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   int wcap = std::max(8, std::min(128, env_int("RS_WAIT_RING", wdef)));
   // whole-prompt prefill (no chunking, m <= 64) takes the lane-per-instance
   // kernel; chunked prefill and larger fleets take the general kernel
-  const bool fast = rs_internal_fast_path(cfg);
+  const bool fast = rs_internal_fast_path(cfg) && !traj;
   if (resident && !fast)
     return fail(RS_ERR_INVALID_ARGUMENT, "streamed inputs need the lane-per-instance kernel");
   const int groups = m_inst <= 32 ? 1 : 2;
@@ -583,6 +603,18 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   kp.predictor_seed = tr->predictor_seed;
   kp.given_bucket = tr->given_bucket;
   kp.resident = resident;
+  if (traj) {  // ClusterConfig::record_trajectory (general kernel)
+    kp.traj = *traj;
+    kp.traj_on = 1;
+    kp.traj_scan = (traj->queue_penalty || traj->reward) ? 1 : 0;
+    kp.r_w = traj->r_w;
+    // RewardConfig::shaping_coefficient(episode_k) (env.hpp:55-63), host libm
+    kp.c_k = traj->shaping == RS_SHAPING_NONE       ? 0.0
+             : traj->shaping == RS_SHAPING_ADDITIVE ? 1.0
+                                                    : traj->gamma * std::exp(-traj->beta_d *
+                                                                             static_cast<double>(
+                                                                                 traj->episode_k));
+  }
   if (cfg->flags & RS_FLAG_PREDICT_INLINE) {
     if (cfg->predictor_mode == RS_PREDICTOR_SIMULATED && !tr->predictor_seed)
       return fail(RS_ERR_INVALID_ARGUMENT, "simulated predictor needs trace->predictor_seed");

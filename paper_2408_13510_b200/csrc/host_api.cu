@@ -107,6 +107,9 @@ __global__ void __launch_bounds__(rs::kWarp * kMlpWarps) mlp_kernel(const __grid
 
 extern "C" rs_status rs_replay_batch(const rs_batch_cfg*, const rs_trace_soa*, rs_req_out*,
                                      rs_replay_stats*, void*, size_t, void*);
+extern "C" rs_status rs_replay_trajectory(const rs_batch_cfg*, const rs_trace_soa*, rs_req_out*,
+                                          rs_replay_stats*, const rs_trajectory*, void*, size_t,
+                                          void*);
 extern "C" rs_status rs_predict_buckets(const rs_batch_cfg*, const rs_trace_soa*, uint8_t*, void*);
 extern "C" rs_status rs_validate_config(const rs_batch_cfg*);
 extern "C" rs_status rs_workspace_size(const rs_batch_cfg*, int32_t, int64_t, size_t*);
@@ -117,10 +120,11 @@ namespace {
 rs_status forward(rs_status s) { return s; }
 }  // namespace
 
-extern "C" {
+namespace {
 
-rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_out* out,
-                               rs_replay_stats* stats, int32_t device) {
+// rs_replay_batch_host / rs_replay_trajectory_host (htraj: host arrays).
+rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_out* out,
+                      rs_replay_stats* stats, const rs_trajectory* htraj, int32_t device) {
   rs_status s = forward(rs_validate_config(cfg));
   if (s != RS_OK) return s;
   if (!tr || !stats) return fail2(RS_ERR_INVALID_ARGUMENT, "null trace/stats");
@@ -168,6 +172,25 @@ rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, 
   const size_t o_st = o; o += al(sizeof(rs_replay_stats) * R);
   const size_t o_ws = o; o += al(ws_bytes);
   const size_t o_fl = o; o += al(4);
+  // trajectory arrays (record_trajectory): one region per requested field
+  const int64_t nrec = htraj ? (int64_t)R * htraj->capacity : 0;
+  const int m = cfg->num_instances;
+  struct TField { const void* host; size_t es, mult, off; };
+  TField tf[12] = {};
+  if (htraj) {
+    const void* hp[12] = {htraj->time_s, htraj->action, htraj->queue_penalty,
+                          htraj->completions, htraj->h, htraj->shaping_term, htraj->reward,
+                          htraj->infeasible_route, htraj->router_queue, htraj->tokens_emitted,
+                          htraj->instance_running, htraj->instance_waiting};
+    const size_t es[12] = {8, 4, 8, 4, 8, 8, 8, 1, 4, 4, 4, 4};
+    for (int k = 0; k < 12; ++k) {
+      tf[k].host = hp[k];
+      tf[k].es = es[k];
+      tf[k].mult = k >= 10 ? (size_t)m : 1;
+      tf[k].off = o;
+      if (hp[k]) o += al(es[k] * tf[k].mult * (size_t)nrec);
+    }
+  }
   DeviceCache& dc = g_cache[device];
   std::lock_guard<std::mutex> lock(dc.mu);
   char* b = nullptr;
@@ -188,7 +211,7 @@ rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, 
   const char* se = getenv("RS_STREAM_INPUTS");
   const int64_t min_stream = se ? atoll(se) : (int64_t)1 << 22;
   const bool stream_in = uniform && n_eq > 0 && min_stream > 0 && N >= min_stream &&
-                         rs_internal_fast_path(cfg);
+                         rs_internal_fast_path(cfg) && !htraj;
   RS_CUDA2(h2d(o_off, tr->offsets, 8ull * (R + 1)));
   if (!stream_in) {
     RS_CUDA2(h2d(o_arr, tr->arrival_s, 8ull * N));
@@ -222,7 +245,19 @@ rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, 
   rs_replay_stats* dstats = reinterpret_cast<rs_replay_stats*>(b + o_st);
 
   dcfg.flags |= RS_FLAG_PREDICT_INLINE;  // predictions drawn inside the replay
-  if (!stream_in) {
+  rs_trajectory dtraj;
+  if (htraj) {
+    dtraj = *htraj;
+    void** dp[12] = {(void**)&dtraj.time_s, (void**)&dtraj.action, (void**)&dtraj.queue_penalty,
+                     (void**)&dtraj.completions, (void**)&dtraj.h, (void**)&dtraj.shaping_term,
+                     (void**)&dtraj.reward, (void**)&dtraj.infeasible_route,
+                     (void**)&dtraj.router_queue, (void**)&dtraj.tokens_emitted,
+                     (void**)&dtraj.instance_running, (void**)&dtraj.instance_waiting};
+    for (int k = 0; k < 12; ++k) *dp[k] = tf[k].host ? (void*)(b + tf[k].off) : nullptr;
+    if ((s = forward(rs_replay_trajectory(&dcfg, &dt, &dout, dstats, &dtraj, b + o_ws, ws_bytes,
+                                          st))) != RS_OK)
+      return s;
+  } else if (!stream_in) {
     if ((s = forward(rs_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st))) !=
         RS_OK)
       return s;
@@ -271,7 +306,7 @@ rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, 
     }
     RS_CUDA2(cudaEventRecord(dc.ev_done, cs));
     s = forward(rs_internal_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st, flag,
-                                         dc.ev_done));
+                                         dc.ev_done, nullptr));
     if (s != RS_OK) {
       cudaStreamSynchronize(cs);
       return s;
@@ -290,6 +325,9 @@ rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, 
     RS_CUDA2(d2h(out->predicted_bucket, o_pb, 1ull * N));
   }
   RS_CUDA2(d2h(stats, o_st, sizeof(rs_replay_stats) * R));
+  for (int k = 0; htraj && k < 12; ++k)
+    if (tf[k].host)
+      RS_CUDA2(d2h(const_cast<void*>(tf[k].host), tf[k].off, tf[k].es * tf[k].mult * (size_t)nrec));
   RS_CUDA2(cudaStreamSynchronize(st));
   // The reference leaves predicted_bucket unset (-1) for requests that never
   // reached the router queue; report those as 255.
@@ -300,6 +338,22 @@ rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, 
     }
   }
   return RS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_out* out,
+                               rs_replay_stats* stats, int32_t device) {
+  return replay_host(cfg, tr, out, stats, nullptr, device);
+}
+
+rs_status rs_replay_trajectory_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr,
+                                    rs_req_out* out, rs_replay_stats* stats,
+                                    const rs_trajectory* traj, int32_t device) {
+  if (!traj) return fail2(RS_ERR_INVALID_ARGUMENT, "null trajectory");
+  return replay_host(cfg, tr, out, stats, traj, device);
 }
 
 rs_status rs_mlp_forward_host(const rs_batch_cfg* cfg, const double* states, int32_t batch,

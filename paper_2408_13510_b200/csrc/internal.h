@@ -10,8 +10,8 @@ bool rs_internal_fast_path(const rs_batch_cfg* cfg);
 // rs_replay_batch with optional streamed inputs: `resident` (device int,
 // may be null) counts the requests of every replay already on the device;
 // `inputs_done` (cudaEvent_t, may be null) is waited on before the
-// percentile pass.
+// percentile pass; `traj` (may be null) turns on record_trajectory.
 rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr,
                                    rs_req_out* out, rs_replay_stats* stats, void* workspace,
                                    size_t workspace_bytes, void* stream, const int* resident,
-                                   void* inputs_done);
+                                   void* inputs_done, const rs_trajectory* traj);

@@ -405,10 +405,11 @@ __device__ inline void running_aggregates(const KParams& P, const Grp& G, int i,
 }
 
 // Instance::step (instance.hpp:203-277) + preempt_if_needed (282-299).
-// Returns the number of completions, or -1 when nothing is admissible.
+// Returns the number of completions, or -1 when nothing is admissible;
+// adds the iteration's IterationOutcome::tokens_emitted to `tokens`.
 template <bool NEED_DBC>
 __device__ inline int inst_step(const KParams& P, const Grp& G, long long off, int i,
-                                InstHot& h) {
+                                InstHot& h, int& tokens) {
   const int l = lane_id();
   if (h.w_cnt > 0 && h.n_run < P.max_batch) admit(P, G, off, i, h);
   if (h.n_run == 0) return -1;  // logic_error, instance.hpp:209-211
@@ -452,6 +453,7 @@ __device__ inline int inst_step(const KParams& P, const Grp& G, long long off, i
           const int excl = incl - x;
           const int take = min(budget, incl) - min(budget, excl);
           emits[k] = v && x == 0;  // co-decoders
+          tokens += __popc(__ballot_sync(kFull, emits[k]));
           e_pm[k] = x - take;
           carry = __shfl_sync(kFull, incl, kWarp - 1);
         }
@@ -464,6 +466,7 @@ __device__ inline int inst_step(const KParams& P, const Grp& G, long long off, i
   } else {
     // decode_batch_time with the running count (instance.hpp:244-245)
     elapsed = __dadd_rn(P.dtb, __dmul_rn(P.dpt, (double)n));
+    tokens += n;
 #pragma unroll
     for (int k = 0; k < kMaxRunChunks; ++k) emits[k] = k * kWarp + l < n;
   }

@@ -40,6 +40,19 @@ __device__ __forceinline__ double capacity_of(const KParams& P, int kv) {
   return v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
 }
 
+// mixing_for (impact.hpp:73-77): prompt_impact (51-59), decode_impact
+// (63-67), mixing_penalty (69-71) against an instance's token mass
+// InstanceLoad::token_sum (39-43), in the reference's operand order.
+__device__ __forceinline__ double mixing_for(const KParams& P, long long p, long long d,
+                                             long long token_sum) {
+  const double pi = (double)p;
+  const double lead = P.prompt_exp == 2 ? __dmul_rn(pi, pi) : pi;
+  const double t_p = __dmul_rn(P.grad1, __dadd_rn(lead, (double)token_sum));
+  const double r_p = t_p <= P.eps_s ? 1.0 : __dsub_rn(1.0, __ddiv_rn(t_p, P.eps_s));
+  const double r_d = __dmul_rn(-P.grad2, (double)(token_sum + p + d));
+  return __dadd_rn(__dmul_rn(P.alpha, r_p), __dmul_rn(__dsub_rn(1.0, P.alpha), r_d));
+}
+
 __device__ __forceinline__ double round2(double x) {  // env.hpp:82
   return __ddiv_rn(round(__dmul_rn(x, 100.0)), 100.0);
 }
@@ -343,13 +356,7 @@ __device__ inline int decide(const KParams& P, const Grp& G, const MlpView& M, R
           const long long p = hr.prompt, d = hr.dhat;
           const double avail = __dmul_rn(P.dtb, (double)f.dleft);
           const double pcost = __dmul_rn(P.tpp, (double)(f.pend + p));
-          const double pi = (double)p;
-          const double lead = P.prompt_exp == 2 ? __dmul_rn(pi, pi) : pi;
-          const double t_p = __dmul_rn(P.grad1, __dadd_rn(lead, (double)f.tok));
-          const double r_p = t_p <= P.eps_s ? 1.0 : __dsub_rn(1.0, __ddiv_rn(t_p, P.eps_s));
-          const double r_d = __dmul_rn(-P.grad2, (double)(f.tok + p + d));
-          const double mix = __dadd_rn(__dmul_rn(P.alpha, r_p),
-                                       __dmul_rn(__dsub_rn(1.0, P.alpha), r_d));
+          const double mix = mixing_for(P, p, d, f.tok);
           const double score = __dsub_rn(__dadd_rn(avail, pcost), __dmul_rn(P.eps_s, mix));
           k = ordered_key(score);
         }
@@ -465,6 +472,111 @@ __device__ inline void write_replay_stats(const KParams& P, const Replay& R, int
   write_replay_stats(P, R, r, warp_lanes(l));
 }
 
+// ---------------------------------------------------- trajectory mode
+// ClusterConfig::record_trajectory: the reward of ClusterSim::step
+// (env.hpp:257-303) and the TickRecord (env.hpp:305-319), per tick.
+
+// heuristic_h (impact.hpp:94-103) of routing the head (p, d_hat) to
+// `action`, over instance_loads() before the enqueue (env.hpp:268-269):
+// the chosen instance's mixing score minus the best, std::max order.
+__device__ inline double traj_heuristic_h(const KParams& P, const Grp& G, int p, int d,
+                                          int action) {
+  double best = 0.0, chosen = 0.0;
+  for (int i = 0; i < P.m; ++i) {
+    const InstHot& h = G.inst[i];
+    const double sc = mixing_for(P, p, d, h.tok_run + h.tok_wait);
+    if (i == 0 || best < sc) best = sc;  // best = std::max(best, sc)
+    if (i == action) chosen = sc;
+  }
+  return __dsub_rn(chosen, best);
+}
+
+// Eq. 3 queue penalty (env.hpp:289-298): sum over the arrived, uncompleted
+// requests in pool-index order of (1/T^)(1 - emitted/d^), T^ =
+// estimate_request_time (latency.hpp:87-92).  Emitted counts come from
+// ov_emit, refreshed here for every running and ring-resident request
+// (overflow entries carry theirs; router-queue entries are 0).  `lo` is
+// the first uncompleted index (monotone).  Sequential fp64 adds in index
+// order, identical on every lane.
+__device__ inline double traj_queue_penalty(const KParams& P, const Grp& G, const Replay& R,
+                                            int& lo) {
+  const int l = lane_id();
+  const long long off = R.off;
+  for (int i = 0; i < P.m; ++i) {
+    const InstHot& h = G.inst[i];
+    for (int j = l; j < h.n_run; j += kWarp)
+      P.ov_emit[off + G.r_req[i * P.rcap + j]] = G.r_emit[i * P.rcap + j];
+    for (int q = l; q < h.w_cnt; q += kWarp) {
+      int sl = h.w_head + q;
+      if (sl >= P.wcap) sl -= P.wcap;
+      P.ov_emit[off + G.w_req[i * P.wcap + sl]] = G.w_emit[i * P.wcap + sl];
+    }
+  }
+  __syncwarp();
+  for (;;) {  // advance past the completed prefix
+    const int j = lo + l;
+    const bool open = j < R.cursor && !(P.o_completion[off + j] >= 0.0);
+    const unsigned b = __ballot_sync(kFull, open || j >= R.cursor);
+    if (b) { lo += __ffs(b) - 1; break; }
+    lo += kWarp;
+  }
+  double acc = 0.0;
+  for (int base = lo; base < R.cursor; base += kWarp) {
+    const int j = base + l;
+    double term = 0.0;
+    bool v = false;
+    if (j < R.cursor) {
+      const long long g = off + j;
+      v = !(P.o_completion[g] >= 0.0);
+      if (v) {
+        const double d_hat = (double)P.ub[P.bucket[g]];
+        const double t_hat = __dadd_rn(__dmul_rn(P.tpp, (double)P.prompt[g]),
+                                       __dmul_rn(P.dtb, d_hat));
+        const double f = __ddiv_rn((double)P.ov_emit[g], d_hat);
+        term = __dmul_rn(__ddiv_rn(1.0, t_hat), __dsub_rn(1.0, f));
+      }
+    }
+    const unsigned vm = __ballot_sync(kFull, v);
+    for (int k = 0; k < kWarp; ++k) {
+      const double tk = __shfl_sync(kFull, term, k);
+      if ((vm >> k) & 1u) acc = __dadd_rn(acc, tk);
+    }
+  }
+  return acc;
+}
+
+// One TickRecord (after ++tick_, env.hpp:303-319) into the trajectory.
+__device__ inline void traj_record(const KParams& P, const Grp& G, const Replay& R, int r,
+                                   int action, int comps, double h, bool infeasible,
+                                   int tokens, int qlen, int& lo) {
+  const rs_trajectory& T = P.traj;
+  double qp = 0.0;
+  if (P.traj_scan) qp = traj_queue_penalty(P, G, R, lo);
+  if (R.tick > T.capacity) return;
+  const long long rec = (long long)r * T.capacity + (R.tick - 1);
+  const int l = lane_id();
+  if (l == 0) {
+    const double shaping = __dmul_rn(P.c_k, h);
+    if (T.time_s) T.time_s[rec] = R.clock;
+    if (T.action) T.action[rec] = action;
+    if (T.queue_penalty) T.queue_penalty[rec] = qp;
+    if (T.completions) T.completions[rec] = comps;
+    if (T.h) T.h[rec] = h;
+    if (T.shaping_term) T.shaping_term[rec] = shaping;
+    if (T.reward)  // env.hpp:300-302
+      T.reward[rec] = __dadd_rn(__dadd_rn(-qp, __dmul_rn(P.r_w, (double)comps)), shaping);
+    if (T.infeasible_route) T.infeasible_route[rec] = infeasible ? 1 : 0;
+    if (T.router_queue) T.router_queue[rec] = qlen;
+    if (T.tokens_emitted) T.tokens_emitted[rec] = tokens;
+  }
+  for (int i = l; i < P.m; i += kWarp) {
+    const InstHot& hi = G.inst[i];
+    if (T.instance_running) T.instance_running[rec * P.m + i] = hi.n_run;
+    if (T.instance_waiting) T.instance_waiting[rec * P.m + i] = hi.w_cnt + hi.o_cnt;
+  }
+  __syncwarp();
+}
+
 template <int POL>
 __device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int r) {
   constexpr bool NEED_DBC = POL == RS_POLICY_RL;
@@ -484,11 +596,13 @@ __device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int
     P.o_completion[g] = -1.0;
     P.o_preempt[g] = 0;
     if (POL == RS_POLICY_MIN_MIN) P.mm_removed[g] = 0;
+    if (P.traj_on) P.ov_emit[g] = 0;  // tokens_emitted of never-routed requests
     const int p = P.prompt[g], d = P.decode[g];
     if (p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens) bad = true;
     if (j > 0 && P.arrival[g] < P.arrival[g - 1]) bad = true;
   }
   bad = __any_sync(kFull, bad);
+  int traj_lo = 0;  // first uncompleted request (reward scan)
   for (int i = l; i < m; i += kWarp) {
     InstHot h;
     h.clock = 0.0;
@@ -546,10 +660,14 @@ __device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int
     R.hash = hash_action(R.hash, action);
     if (action < 0 || action > m) { R.status = RS_REPLAY_BAD_ACTION; break; }
     const double t1 = __dadd_rn(R.clock, P.delta_t);
+    double th = 0.0;  // RewardBreakdown::h
+    bool infeasible = false;
     if (action < m && has_head) {
       if ((long long)hr.prompt + hr.tru > P.kv_cap) {
         R.infeasible++;  // env.hpp:262-267: flagged, stays queued
+        infeasible = true;
       } else {
+        if (P.traj_on && l == 0) th = traj_heuristic_h(P, G, hr.prompt, hr.dhat, action);
         if (POL == RS_POLICY_MIN_MIN && R.nfront > 0) {
           if (l == 0)
             for (int k = 0; k + 1 < R.nfront; ++k) G.front[k] = G.front[k + 1];
@@ -572,7 +690,7 @@ __device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int
       }
     }
     // run_until(t1) for every instance, index order (independent)
-    int comps = 0;
+    int comps = 0, tokens = 0;
     for (int g = 0; g < m && R.status == RS_REPLAY_FINISHED; g += kWarp) {
       const int i = g + l;
       bool busy = false;
@@ -591,7 +709,7 @@ __device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int
         InstHot h = load_inst(G, ii);
         const int w0 = h.w_cnt + h.o_cnt;
         while (h.clock < t1 && (h.n_run > 0 || h.w_cnt > 0)) {
-          const int c = inst_step<NEED_DBC>(P, G, R.off, ii, h);
+          const int c = inst_step<NEED_DBC>(P, G, R.off, ii, h, tokens);
           if (c < 0) {
             R.status = RS_REPLAY_NOT_ADMISSIBLE;
             R.err_inst = ii;
@@ -612,6 +730,8 @@ __device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int
     R.tick++;
     R.sum_q += queue_len<POL>(R);
     R.sum_w += R.total_wait;
+    if (P.traj_on)
+      traj_record(P, G, R, r, action, comps, th, infeasible, tokens, queue_len<POL>(R), traj_lo);
   }
   if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
 

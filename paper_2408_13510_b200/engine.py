@@ -9,6 +9,9 @@ Reference names are kept so harness code reads the same:
                                                  on an unknown name, as invalid_argument)
   ClusterSim(cfg, trace) + run_policy(policy,    BatchSim(cfg, traces, seeds).run_policy(
     max_ticks) (env.hpp:174-194, 326-337)          policy, max_ticks) for a whole batch
+  record_trajectory + trajectory()               BatchSim.run_trajectory(policy, capacity,
+    (env.hpp:131, 203, 305-319)                    reward, episode_k)
+  RewardConfig (env.hpp:40-71)                   RewardConfig
   evaluate_policy over seeds                     BatchSim over the seed batch
     (experiment.hpp:648-670)
   build_workload (experiment.hpp:291-305)        build_workload(seed, n, rate, ...)
@@ -82,6 +85,15 @@ class ClusterConfig:
         c.predictor_mode = {"simulated": abi.PRED_SIMULATED, "empirical": abi.PRED_EMPIRICAL,
                             "given": abi.PRED_GIVEN}[self.predictor_mode]
         return c
+
+
+@dataclass
+class RewardConfig:
+    """RewardConfig (env.hpp:40-71) with the reference defaults."""
+    r_w: float = 60.0
+    gamma: float = 0.99
+    beta_d: float = 0.5
+    shaping: str = "guided"   # ShapingMode: none | additive | guided
 
 
 @dataclass
@@ -173,6 +185,25 @@ class BatchSim:
 
     def run_policy(self, policy: str, max_ticks: int = 10_000_000, agent=None,
                    epsilon: float = 0.0) -> BatchResult:
+        return self._run(policy, max_ticks, agent, epsilon, None)
+
+    def run_trajectory(self, policy: str, capacity: int, reward: RewardConfig | None = None,
+                       episode_k: int = 0, max_ticks: int = 10_000_000, agent=None,
+                       epsilon: float = 0.0, fields=None):
+        """run_policy with ClusterConfig::record_trajectory (env.hpp:131): also
+        returns every replay's ClusterSim::trajectory() (env.hpp:203) as
+        {TickRecord field: array [R, capacity(, m)]}; replay r's tick t is
+        row t-1 (ticks past `capacity` run but are not recorded)."""
+        reward = reward or RewardConfig()
+        t, arrays = abi.make_trajectory(capacity, self.traces.num_replays,
+                                        self.cfg.num_instances, r_w=reward.r_w,
+                                        gamma=reward.gamma, beta_d=reward.beta_d,
+                                        shaping=reward.shaping, episode_k=episode_k,
+                                        fields=fields)
+        res = self._run(policy, max_ticks, agent, epsilon, t)
+        return res, arrays
+
+    def _run(self, policy, max_ticks, agent, epsilon, traj) -> BatchResult:
         pid = make_policy(policy)
         c = self.cfg.to_abi(policy)
         c.policy = pid
@@ -196,8 +227,13 @@ class BatchSim:
         out = abi.ReqOut(res.instance.ctypes.data, res.routed.ctypes.data, res.first.ctypes.data,
                          res.completion.ctypes.data, res.preemptions.ctypes.data,
                          res.predicted.ctypes.data)
-        abi.check(self.lib, self.lib.rs_replay_batch_host(C.byref(c), C.byref(tr), C.byref(out),
-                                                          res.stats.ctypes.data, self.device))
+        if traj is None:
+            abi.check(self.lib, self.lib.rs_replay_batch_host(
+                C.byref(c), C.byref(tr), C.byref(out), res.stats.ctypes.data, self.device))
+        else:
+            abi.check(self.lib, self.lib.rs_replay_trajectory_host(
+                C.byref(c), C.byref(tr), C.byref(out), res.stats.ctypes.data, C.byref(traj),
+                self.device))
         del keep
         return res
 

@@ -9,6 +9,11 @@ exists; the outputs are committed and the GPU box only reads them.
                         byte-identical to proj/tests/golden/mini_summary.json.
  * replays.npz        — per-request outputs + per-replay stats of the
                         reference ClusterSim::run_policy for the cases below.
+ * trajectories.npz   — ClusterSim::trajectory() (record_trajectory on: the
+                        Eq. 3 reward breakdown + TickRecords, env.hpp:251-319)
+                        for traj_cases(), under several RewardConfigs.
+
+    python tests/golden/make_golden.py [--traj-only]
 """
 from __future__ import annotations
 
@@ -75,7 +80,66 @@ def cases():
     return out
 
 
+def traj_cases():
+    """(name, cfg, trace, predictor_seed, policy_seed, agent, reward) tuples."""
+    out = []
+    tr = O.ref_generate(21, 300, 20.0)
+    ps = abi.mix_seed(21, 0x9DED)
+    out.append(("jsq_default", abi.default_config("jsq", 4), tr, ps, 0, None, {}))
+    out.append(("wa_guided_k2", abi.default_config("workload_aware", 4), tr, ps, 0, None,
+                {"shaping": "guided", "episode_k": 2}))
+    out.append(("rr_additive_rw30", abi.default_config("round_robin", 4),
+                O.ref_generate(22, 250, 45.0), abi.mix_seed(22, 0x9DED), 0, None,
+                {"shaping": "additive", "r_w": 30.0}))
+    out.append(("minmin_none", abi.default_config("min_min", 3), O.ref_generate(23, 250, 60.0),
+                abi.mix_seed(23, 0x9DED), 0, None, {"shaping": "none"}))
+    c = abi.default_config("decode_balancer", 3)
+    c.chunk_size = 96
+    out.append(("chunk96_db", c, O.ref_generate(24, 250, 30.0), abi.mix_seed(24, 0x9DED), 0, None,
+                {"episode_k": 5}))
+    rng = np.random.default_rng(4)
+    rows = [(i * 0.05, int(rng.integers(100, 600)), int(rng.integers(600, 999)),
+             int(rng.integers(0, 5))) for i in range(120)]
+    c = abi.default_config("jsq", 2)
+    c.kv_capacity_tokens = 6000
+    for t in range(5):
+        c.accuracy[t] = 0.0
+    out.append(("preempt_jsq", c, O.make_trace(rows), 6, 0, None, {"shaping": "additive"}))
+    params = O.ref_agent_params(27, 5, 64, 42)
+    out.append(("rl_eps", abi.default_config("rl", 4), O.ref_generate(25, 200, 30.0),
+                abi.mix_seed(25, 0x9DED), 77, ([27, 64, 64, 5], params), {"episode_k": 1}))
+    return out
+
+
+def main_traj():
+    arrays = {}
+    meta = {}
+    for name, cfg, tr, ps, qs, agent, reward in traj_cases():
+        keep = None
+        if agent is not None:
+            keep = abi.set_rl(cfg, agent[0], agent[1])
+            arrays[f"{name}.params"] = agent[1]
+            cfg.rl_epsilon = 0.2
+        res, traj = O.ref_trajectory(cfg, tr, ps, qs, reward=reward)
+        arrays.update({f"{name}.arrival": tr.arrival, f"{name}.prompt": tr.prompt,
+                       f"{name}.decode": tr.decode, f"{name}.task": tr.task,
+                       f"{name}.stats": res.stats, f"{name}.completion": res.completion,
+                       f"{name}.cfg": np.frombuffer(bytes(cfg), np.uint8)})
+        for k, v in traj.items():
+            arrays[f"{name}.traj.{k}"] = v
+        meta[name] = {"predictor_seed": ps, "policy_seed": qs, "reward": reward,
+                      "dims": agent[0] if agent else None,
+                      "ticks": int(res.stats["ticks"][0])}
+        del keep
+        print(f"traj {name:20s} ticks={meta[name]['ticks']:8d}")
+    np.savez_compressed(HERE / "trajectories.npz", **arrays)
+    (HERE / "trajectories.json").write_text(json.dumps(meta, indent=1) + "\n")
+
+
 def main():
+    main_traj()
+    if "--traj-only" in sys.argv:
+        return
     lib = O.ref_lib()
     buf = C.create_string_buffer(1 << 16)
     assert lib.ref_golden_summary(buf, len(buf), 1) == 0

@@ -46,6 +46,8 @@ def ora_lib() -> C.CDLL:
             C.c_uint64, C.c_void_p]
         lib.ora_mlp_forward.argtypes = [P(abi.BatchCfg), C.c_void_p, C.c_int32, C.c_void_p,
                                         C.c_void_p]
+        lib.ora_run_trajectory.argtypes = [P(abi.BatchCfg), C.c_int64] + [C.c_void_p] * 5 + [
+            C.c_uint64, C.c_uint64] + [C.c_void_p] * 7 + [P(abi.Trajectory)]
         lib.ora_mt19937_64.argtypes = [C.c_uint64, C.c_int64, C.c_void_p]
         lib.ora_mix_seed.restype = C.c_uint64
         lib.ora_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
@@ -69,6 +71,8 @@ def ref_lib() -> C.CDLL:
                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         lib.ref_run_replay.argtypes = [P(abi.BatchCfg), C.c_int64] + [C.c_void_p] * 4 + [
             C.c_uint64, C.c_uint64] + [C.c_void_p] * 8 + [C.c_int64]
+        lib.ref_run_trajectory.argtypes = [P(abi.BatchCfg), C.c_int64] + [C.c_void_p] * 4 + [
+            C.c_uint64, C.c_uint64] + [C.c_void_p] * 7 + [P(abi.Trajectory)]
         lib.ref_run_batch.restype = C.c_double
         lib.ref_run_batch.argtypes = [P(abi.BatchCfg), C.c_int32] + [C.c_void_p] * 7 + [
             C.c_int32, C.c_void_p]
@@ -233,4 +237,55 @@ def compare(a: ReplayResult, b: ReplayResult, exact_times: bool = True) -> list[
                                b.actions[: min(len(a.actions), len(b.actions))])[0]) \
             if min(len(a.actions), len(b.actions)) else 0
         errs.append(f"actions differ first at tick {i}")
+    return errs
+
+
+def _run_traj(fn, cfg, tr: Trace, predictor_seed, policy_seed, capacity, reward, given=None):
+    """One replay with record_trajectory: (ReplayResult, {field: [capacity(, m)]})."""
+    n = tr.n
+    out = _alloc(max(n, 1))
+    t, arrays = abi.make_trajectory(capacity, 1, cfg.num_instances, **(reward or {}))
+    args = [C.byref(cfg), n, tr.arrival.ctypes.data, tr.prompt.ctypes.data,
+            tr.decode.ctypes.data, tr.task.ctypes.data]
+    if given is not None:
+        args.append(abi.ptr(given))
+    args += [predictor_seed, policy_seed, out.instance.ctypes.data, out.routed.ctypes.data,
+             out.first.ctypes.data, out.completion.ctypes.data, out.preemptions.ctypes.data,
+             out.predicted.ctypes.data, out.stats.ctypes.data, C.byref(t)]
+    if fn(*args) != 0:
+        raise RuntimeError("checker failed")
+    for f in ("instance", "routed", "first", "completion", "preemptions", "predicted"):
+        setattr(out, f, getattr(out, f)[:n])
+    k = int(min(out.stats["ticks"][0], capacity))
+    return out, {name: a[0, :k] for name, a in arrays.items()}
+
+
+def ora_trajectory(cfg, tr: Trace, predictor_seed=1, policy_seed=0, capacity=200_000,
+                   reward=None):
+    return _run_traj(ora_lib().ora_run_trajectory, cfg, tr, predictor_seed, policy_seed,
+                     capacity, reward, given=np.zeros(max(tr.n, 1), np.uint8))
+
+
+def ref_trajectory(cfg, tr: Trace, predictor_seed=1, policy_seed=0, capacity=200_000,
+                   reward=None):
+    try:
+        return _run_traj(ref_lib().ref_run_trajectory, cfg, tr, predictor_seed, policy_seed,
+                         capacity, reward)
+    except RuntimeError as e:
+        raise RuntimeError(f"{e}: {ref_error()}") from None
+
+
+def compare_trajectory(a: dict, b: dict) -> list[str]:
+    """Bitwise differences between two trajectories ([] when identical)."""
+    errs = []
+    for name in a:
+        x, y = a[name], b[name]
+        if x.shape != y.shape:
+            errs.append(f"{name}: shape {x.shape} vs {y.shape}")
+            continue
+        bad = (x.view(np.uint64) != y.view(np.uint64)) if x.dtype == np.float64 else (x != y)
+        if bad.any():
+            i = np.argwhere(bad)[0]
+            errs.append(f"{name} differs at {tuple(i)}: {x[tuple(i)]!r} vs {y[tuple(i)]!r} "
+                        f"({int(bad.sum())} total)")
     return errs
