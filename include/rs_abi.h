@@ -372,6 +372,29 @@ rs_status rs_generate_mixture_batch(const rs_profile* profile,
 rs_status rs_mlp_random_init(const int32_t* dims, int32_t num_layers, uint64_t seed,
                              double* params_out);
 
+/* ---- host-side report layer (one replay) ------------------------------- */
+
+/* compute_metrics + emit_report (metrics.hpp:84-238) for one replay of a
+ * finished batch: writes `dir`/summary.json (report_to_json(...).dump(2),
+ * byte-identical to the reference's nlohmann serialisation), requests.csv and
+ * timeseries.csv ("%.17g" doubles, format_double).  Inputs are the replay's
+ * slice of the trace and of the per-request outputs (host arrays), its
+ * rs_replay_stats record (the device's sums and percentiles are used), and
+ * optionally its trajectory (host arrays, record t-1 for tick t, traj_len
+ * records): with traj == NULL the report is that of record_trajectory =
+ * false (mean_router_queue / mean_instance_waiting 0, timeseries.csv
+ * header only), as run_matrix / evaluate_policy produce.
+ * RS_ERR_INVALID_ARGUMENT when no request completed (compute_metrics'
+ * invalid_argument) or a file cannot be written (emit_report's
+ * runtime_error). */
+rs_status rs_emit_report(const char* dir, const rs_batch_cfg* cfg, int64_t n,
+                         const double* arrival_s, const int32_t* prompt_tokens,
+                         const int32_t* decode_tokens, const uint8_t* task,
+                         const int32_t* instance, const double* routed_s,
+                         const double* first_token_s, const double* completion_s,
+                         const int32_t* preemptions, const rs_replay_stats* stats,
+                         const rs_trajectory* traj, int64_t traj_len);
+
 /* mix_seed (rng.hpp:11-16). */
 uint64_t rs_mix_seed(uint64_t seed, uint64_t stream);
 

@@ -463,6 +463,62 @@ int ref_run_trajectory(const rs_batch_cfg* cfg, int64_t n, const double* arrival
   }
 }
 
+// One replay (record_trajectory as given) through run_policy, then the
+// reference's own compute_metrics + emit_report (metrics.hpp:84-238) into
+// `dir`, as cmd_run does (routesim_cli.cpp:28-40).  Returns 0, or -1 (error
+// text in ref_last_error; "no completed requests" included).
+int ref_emit_report(const rs_batch_cfg* cfg, int64_t n, const double* arrival,
+                    const int32_t* prompt, const int32_t* decode, const uint8_t* task,
+                    uint64_t predictor_seed, uint64_t policy_seed, int32_t record_trajectory,
+                    const rs_trajectory* reward, const char* dir) {
+  try {
+    if (!check_cfg(*cfg)) return -1;
+    std::unique_ptr<DqnAgent> agent;
+    if (cfg->policy == RS_POLICY_RL) agent = make_agent(*cfg);
+    ArrivalTrace trace;
+    trace.requests.resize(static_cast<std::size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      Request& r = trace.requests[static_cast<std::size_t>(i)];
+      r.id = static_cast<std::uint64_t>(i);
+      r.arrival_time_s = arrival[i];
+      r.prompt_tokens = prompt[i];
+      r.true_decode_tokens = decode[i];
+      r.task = static_cast<TaskKind>(task[i]);
+    }
+    ClusterConfig cc = to_cluster(*cfg, predictor_seed);
+    cc.record_trajectory = record_trajectory != 0;
+    if (reward) {
+      cc.reward.r_w = reward->r_w;
+      cc.reward.gamma = reward->gamma;
+      cc.reward.beta_d = reward->beta_d;
+      cc.reward.shaping = static_cast<ShapingMode>(reward->shaping);
+      cc.episode_k = reward->episode_k;
+    }
+    ClusterSim sim(cc, std::move(trace));
+    std::unique_ptr<RoutingPolicy> pol;
+    HardwareProfile prof = cc.profile;
+    static const char* names[] = {"round_robin", "dedicated_small_large", "decode_balancer",
+                                  "jsq", "max_capacity", "min_min", "earliest_available"};
+    if (cfg->policy >= 0 && cfg->policy < 7) {
+      pol = make_policy(names[cfg->policy], prof, cc.thresholds);
+    } else if (cfg->policy == RS_POLICY_WORKLOAD_AWARE) {
+      pol = std::make_unique<WorkloadAwarePolicy>(sim, prof, cc.impact);
+    } else if (cfg->rl_epsilon > 0.0) {
+      pol = std::make_unique<ActPolicy>(*agent, cc.state_scheme, policy_seed);
+    } else {
+      pol = std::make_unique<RlPolicy>(*agent, cc.state_scheme);
+    }
+    sim.run_policy(*pol, cfg->max_ticks);
+    auto rep = compute_metrics(sim.pool(), cc.profile, cc.thresholds, sim.trajectory(),
+                               sim.tokens_per_second());
+    emit_report(rep, sim.trajectory(), dir);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // CPU baseline: replays r in [0, R) of a CSR batch on `threads` host threads
 // (atomic work counter), outputs per replay stats only.  Returns wall seconds
 // (excluding nothing but thread start) or -1 on error.

@@ -328,7 +328,7 @@ EXPORTED_SYMBOLS = (
     "rs_replay_batch", "rs_replay_batch_host", "rs_mlp_forward_host",
     "rs_generate_mixture", "rs_generate_mixture_batch", "rs_mix_seed",
     "rs_heavy_decode_cutoff", "rs_host_alloc", "rs_host_free", "rs_mlp_random_init",
-    "rs_replay_trajectory", "rs_replay_trajectory_host",
+    "rs_replay_trajectory", "rs_replay_trajectory_host", "rs_emit_report",
 )
 
 
@@ -349,6 +349,8 @@ def _declare(lib: C.CDLL) -> None:
                                          P(Trajectory), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.rs_replay_trajectory_host.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,
                                               P(Trajectory), C.c_int32]
+    lib.rs_emit_report.argtypes = [C.c_char_p, P(BatchCfg), C.c_int64] + [C.c_void_p] * 10 + [
+        P(Trajectory), C.c_int64]
     lib.rs_mlp_forward_host.argtypes = [P(BatchCfg), C.c_void_p, C.c_int32, C.c_void_p,
                                         C.c_void_p, C.c_int32]
     lib.rs_generate_mixture.argtypes = [P(Profile), P(Thresholds), C.c_void_p, C.c_uint64,

@@ -1,4 +1,6 @@
-"""Per-replay report in the reference's summary.json shape (metrics.hpp:84-194).
+"""Per-replay report in the reference's summary.json shape (metrics.hpp:84-194),
+and emit_report (metrics.hpp:197-238) through the engine library's C ABI
+(rs_emit_report: byte-identical summary.json / requests.csv / timeseries.csv).
 
 The fp64 sums are the engine's own sequential, pool-index-order sums
 (rs_replay_stats), so means are bit-identical to compute_metrics; the
@@ -7,9 +9,13 @@ outputs (aggregate_of, metrics.hpp:62-80).
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
+import os
 
 import numpy as np
+
+from . import abi
 
 
 def nearest_rank(sorted_values: np.ndarray, q: float) -> float:
@@ -69,3 +75,32 @@ def summary(arrival, decode, routed, first, completion, preemptions, stats, num_
         "total_preemptions": int(stats["total_preemptions"]),
     }
     return out
+
+
+def emit_report(directory, cfg: abi.BatchCfg, arrival, prompt, decode, task, instance, routed,
+                first, completion, preemptions, stats, trajectory: dict | None = None) -> None:
+    """emit_report(compute_metrics(...), trajectory, dir) for ONE replay
+    (metrics.hpp:84-238), through rs_emit_report.  `stats` is the replay's
+    STATS_DTYPE record; `trajectory` its {TickRecord field: array} (the
+    replay's row of BatchSim.run_trajectory, trimmed to its tick count) or
+    None for a record_trajectory = false report."""
+    lib = abi.load_library()
+    c = lambda a, dt: np.ascontiguousarray(a, dtype=dt)
+    arrs = [c(arrival, np.float64), c(prompt, np.int32), c(decode, np.int32), c(task, np.uint8),
+            c(instance, np.int32), c(routed, np.float64), c(first, np.float64),
+            c(completion, np.float64), c(preemptions, np.int32)]
+    st = np.ascontiguousarray(np.asarray(stats).reshape(-1)[:1], dtype=abi.STATS_DTYPE)
+    t = None
+    k = 0
+    keep = []
+    if trajectory is not None:
+        t = abi.Trajectory()
+        for name, dt, _ in abi.TRAJ_FIELDS:
+            if name in trajectory:
+                a = np.ascontiguousarray(trajectory[name], dtype=dt)
+                keep.append(a)
+                setattr(t, name, a.ctypes.data)
+                k = int(a.shape[0])
+    abi.check(lib, lib.rs_emit_report(os.fsencode(str(directory)), C.byref(cfg), len(arrs[0]),
+                                      *[a.ctypes.data for a in arrs], st.ctypes.data,
+                                      C.byref(t) if t is not None else None, k))

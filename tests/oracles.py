@@ -289,3 +289,21 @@ def compare_trajectory(a: dict, b: dict) -> list[str]:
             errs.append(f"{name} differs at {tuple(i)}: {x[tuple(i)]!r} vs {y[tuple(i)]!r} "
                         f"({int(bad.sum())} total)")
     return errs
+
+
+def ref_emit_report(cfg, tr: Trace, directory, predictor_seed=1, policy_seed=0,
+                    record_trajectory=True, reward=None):
+    """The reference's compute_metrics + emit_report of one replay into `directory`."""
+    lib = ref_lib()
+    lib.ref_emit_report.argtypes = [C.POINTER(abi.BatchCfg), C.c_int64] + [C.c_void_p] * 4 + [
+        C.c_uint64, C.c_uint64, C.c_int32, C.POINTER(abi.Trajectory), C.c_char_p]
+    t = None  # None: to_cluster's RewardConfig (shaping none)
+    if reward is not None:
+        t, _ = abi.make_trajectory(0, 1, cfg.num_instances, fields=(), **reward)
+    rc = lib.ref_emit_report(C.byref(cfg), tr.n, tr.arrival.ctypes.data, tr.prompt.ctypes.data,
+                             tr.decode.ctypes.data, tr.task.ctypes.data, predictor_seed,
+                             policy_seed, 1 if record_trajectory else 0,
+                             C.byref(t) if t is not None else None,
+                             os.fsencode(str(directory)))
+    if rc != 0:
+        raise RuntimeError(ref_error())
