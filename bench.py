@@ -462,7 +462,7 @@ def main():
         "kernel_ms": {"replay_batch": replay_s * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "rs::replay_fast_kernel (+ percentile_kernel, timed together)",
+                     "kernel": "rs::replay_fast_kernel (+ stats_kernel, timed together)",
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "peak_source": peak_src},
         "clocks": clk.summary(),

@@ -784,19 +784,21 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   rs_status s2 = launch_kernel(pl.kern, kp, pl.wpb, rs::kWarp / pl.width, pl.block_smem,
                                tr->num_replays, st);
   if (s2 != RS_OK) return s2;
-  // nearest-rank percentiles (metrics.hpp:62-80), one CTA per replay
+  // compute_metrics aggregates (metrics.hpp:62-162), one CTA per replay
   if (inputs_done) RS_CUDA(cudaStreamWaitEvent(st, (cudaEvent_t)inputs_done, 0));
   rs::StatsParams sp;
   sp.num_replays = tr->num_replays;
   sp.offsets = kp.offsets;
   sp.arrival = kp.arrival;
   sp.decode = kp.decode;
+  sp.routed = kp.o_routed;
   sp.first = kp.o_first;
   sp.completion = kp.o_completion;
+  sp.preempt = kp.o_preempt;
   sp.stats = stats;
   {
     const int grid = std::max(1, std::min(tr->num_replays, sms * 8));
-    rs::percentile_kernel<<<grid, rs::kStatsThreads, 0, st>>>(sp);
+    rs::stats_kernel<<<grid, rs::kStatsThreads, 0, st>>>(sp);
     RS_CUDA(cudaGetLastError());
   }
   return RS_OK;

@@ -378,10 +378,19 @@ __device__ __forceinline__ void inject_fast(const KParams& P, Replay& R, unsigne
   }
 }
 
-// Returns true when the replay must be re-run instance-sequentially.
+// Outcome of one pass over a replay.
+enum FastRun { kDone = 0, kRerunSeq = 1, kRerunInit = 2 };
+
+// `init` writes the reference's "not yet" values (-1) into the instance /
+// routed / first-token / completion outputs up front.  A replay that
+// finishes overwrites every one of them, so the first pass skips those
+// writes (32 -> 4 B/request of initialisation traffic) and a replay that
+// ends unfinished (livelock, max_ticks, errors: rare) is re-run with init.
+// `seq` steps instances one at a time in index order (exact stop point of a
+// "nothing admissible" error).
 template <int POL, int G, int W>
-__device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const MlpView& M, int r,
-                                bool seq, const Lanes<W>& L) {
+__device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const MlpView& M, int r,
+                                   bool seq, bool init, const Lanes<W>& L) {
   const int l = L.l;
   Replay R;
   R.off = P.offsets[r];
@@ -394,10 +403,12 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
   int vmax = 0;
   for (int j = l; j < R.n; j += W) {
     const long long g = off + j;
-    P.o_instance[g] = -1;
-    P.o_routed[g] = -1.0;
-    P.o_first[g] = -1.0;
-    P.o_completion[g] = -1.0;
+    if (init) {
+      P.o_instance[g] = -1;
+      P.o_routed[g] = -1.0;
+      P.o_first[g] = -1.0;
+      P.o_completion[g] = -1.0;
+    }
     P.o_preempt[g] = 0;
     if (POL == RS_POLICY_MIN_MIN) P.mm_removed[g] = 0;
     if (P.resident) continue;  // streamed inputs: validated per window on load
@@ -623,7 +634,7 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
             if (S[g].n == 0) err = min(err, g * W + l);
         err = L.min(err);
         if (err != kBig) {
-          if (!seq) return true;  // exact stop point needs index order: re-run
+          if (!seq) return kRerunSeq;  // exact stop point needs index order: re-run
           R.status = RS_REPLAY_NOT_ADMISSIBLE;
           R.err_inst = err;
           break;
@@ -673,8 +684,9 @@ __device__ bool run_replay_fast(const KParams& P, int gw, char* gbase, const Mlp
     R.sum_w += R.total_wait;
   }
   if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
+  if (!init && R.status != RS_REPLAY_FINISHED) return kRerunInit;
   write_replay_stats(P, R, r, L);
-  return false;
+  return kDone;
 }
 
 template <int POL, int G, int W>
@@ -707,8 +719,8 @@ __global__ void __launch_bounds__(256) replay_fast_kernel(const __grid_constant_
     if (L.l == 0) r = atomicAdd(P.work_counter, 1);
     r = L.shfl(r, 0);
     if (r >= P.num_replays) break;
-    if (run_replay_fast<POL, G, W>(P, gw, gbase, M, r, false, L))
-      run_replay_fast<POL, G, W>(P, gw, gbase, M, r, true, L);
+    const FastRun o = run_replay_fast<POL, G, W>(P, gw, gbase, M, r, false, false, L);
+    if (o != kDone) run_replay_fast<POL, G, W>(P, gw, gbase, M, r, o == kRerunSeq, true, L);
   }
 }
 

@@ -372,70 +372,15 @@ __device__ inline int decide(const KParams& P, const Grp& G, const MlpView& M, R
   }
 }
 
-// Per-replay statistics (compute_metrics, metrics.hpp:84-162): fp64 sums are
-// sequential in pool-index order, bit-identical to the reference.
+// Per-replay record: the replay-state fields (ClusterSim accessors, the
+// decision hash, the time-average numerators).  The per-request aggregates
+// of compute_metrics (metrics.hpp:84-162: sequential pool-index-order sums,
+// nearest-rank percentiles) are filled by stats_kernel (stats.cuh), which
+// runs right after the replay kernel.
 template <int W>
 __device__ inline void write_replay_stats(const KParams& P, const Replay& R, int r, const Lanes<W>& L) {
-  const int l = L.l;
-  double se = 0.0, st = 0.0, sb = 0.0, sw = 0.0;
-  long long tbtc = 0, pre = 0, tok = 0;
-  double fa = __longlong_as_double(0x7fefffffffffffffll), lc = 0.0;
-  for (int b0 = 0; b0 < R.n; b0 += W) {
-    const int j = b0 + l;
-    const bool v = j < R.n;
-    const long long g = R.off + j;
-    const double comp = v ? P.o_completion[g] : -1.0;
-    const bool c = comp >= 0.0;
-    double e = 0.0, t = 0.0, tb = 0.0, w = 0.0, arr = 0.0;
-    bool htb = false, hw = false;
-    if (c) {
-      arr = P.arrival[g];
-      const double first = P.o_first[g];
-      const double routed = P.o_routed[g];
-      const int d = P.decode[g];  // tokens_emitted at completion
-      e = __dsub_rn(comp, arr);
-      t = __dsub_rn(first, arr);
-      if (d >= 2) {
-        htb = true;
-        tb = __ddiv_rn(__dsub_rn(comp, first), (double)(d - 1));
-      }
-      if (routed >= 0.0) {
-        hw = true;
-        w = __dsub_rn(routed, arr);
-      }
-      pre += P.o_preempt[g];
-      tok += d;
-      tbtc += htb;
-      fa = arr < fa ? arr : fa;
-      lc = comp > lc ? comp : lc;
-    }
-    const unsigned cm = L.ballot(c), tm = L.ballot(htb),
-                   wm = L.ballot(hw);
-    // sequential sums in pool-index order (bit-identical to compute_metrics)
-    for (int k = 0; k < W; ++k) {
-      const double ek = L.shfl(e, k), tk = L.shfl(t, k);
-      const double bk = L.shfl(tb, k), wk = L.shfl(w, k);
-      if ((cm >> k) & 1u) {
-        se = __dadd_rn(se, ek);
-        st = __dadd_rn(st, tk);
-      }
-      if ((tm >> k) & 1u) sb = __dadd_rn(sb, bk);
-      if ((wm >> k) & 1u) sw = __dadd_rn(sw, wk);
-    }
-  }
-  pre = L.sum_ll(pre);
-  tok = L.sum_ll(tok);
-  tbtc = L.sum_ll(tbtc);
-  {
-    unsigned long long a = (unsigned long long)__double_as_longlong(fa);
-    a = L.min_u64(a);  // non-negative doubles order like their bits
-    fa = __longlong_as_double((long long)a);
-    unsigned long long b = (unsigned long long)__double_as_longlong(lc);
-    b = L.max_u64(b);
-    lc = __longlong_as_double((long long)b);
-  }
-  if (l == 0) {
-    rs_replay_stats s;
+  if (L.l == 0) {
+    rs_replay_stats& s = P.stats[r];
     s.ticks = R.tick;
     s.routed = R.routed;
     s.infeasible = R.infeasible;
@@ -443,27 +388,10 @@ __device__ inline void write_replay_stats(const KParams& P, const Replay& R, int
     s.decision_hash = R.hash;
     s.sum_router_queue = R.sum_q;
     s.sum_instance_waiting = R.sum_w;
-    s.total_preemptions = pre;
-    s.total_tokens = tok;
-    s.tbt_count = tbtc;
     s.clock = R.clock;
-    s.total_e2e_s = se;
-    s.total_ttft_s = st;
-    s.total_tbt_s = sb;
-    s.total_router_wait_s = sw;
-    s.first_arrival_s = fa;
-    s.last_completion_s = lc;
-    s.makespan_s = __dsub_rn(lc, fa);
-    s.e2e_p50 = s.e2e_p90 = s.e2e_p99 = 0.0;
-    s.ttft_p50 = s.ttft_p90 = s.ttft_p99 = 0.0;
-    s.tbt_p50 = s.tbt_p90 = s.tbt_p99 = 0.0;
     s.status = R.status;
     s.error_instance = R.err_inst;
-    s.percentiles_valid = 0;
-    s._pad0 = 0;
     s.injected = R.cursor;
-    for (int k = 0; k < 4; ++k) s._pad[k] = 0;
-    P.stats[r] = s;
   }
   L.sync();
 }

@@ -45,7 +45,7 @@ def summary(arrival, decode, routed, first, completion, preemptions, stats, num_
     tbt = (completion[done][has_tbt] - first[done][has_tbt]) / (dd[has_tbt] - 1).astype(np.float64)
     ticks = int(stats["ticks"])
     if int(stats["percentiles_valid"]):
-        # device nearest-rank selections (percentile_kernel, stats.cuh)
+        # device nearest-rank selections (stats_kernel, stats.cuh)
         def _dev(name, n, total):
             return {"mean": total / n if n else 0.0, "p50": float(stats[f"{name}_p50"]),
                     "p90": float(stats[f"{name}_p90"]), "p99": float(stats[f"{name}_p99"]),
