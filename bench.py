@@ -468,6 +468,25 @@ def main():
         "clocks": clk.summary(),
         "trace_gen_s": t_gen,
     }
+    rl_cells = [(c, st, ms) for c, st, ms in zip(cells, cell_stats, cell_ms) if c["policy"] == "rl"]
+    if rl_cells:
+        # Q-network forward (mlp.hpp:54-68) once per decision (RlPolicy::decide
+        # runs every tick): 2 FLOP per MAC of the dense (6m+3)-64-64-(m+1) net,
+        # issued as separately rounded DMUL + DADD (bit-exact, -fmad=false);
+        # peak = the measured DMUL+DADD rate (profiles/fp64_peak.json).
+        dims = agent_for(m)[0]
+        macs = sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
+        flop = sum(2.0 * macs * float(st["ticks"].sum()) for _, st, _ in rl_cells)
+        sec = sum(ms for _, _, ms in rl_cells) / 1e3
+        fp = ROOT / "profiles" / "fp64_peak.json"
+        fpeak = json.loads(fp.read_text())["fp64_tflops_mul_add"] if fp.exists() else None
+        line["roofline_fp64_qnet"] = {
+            "bound": "fp64", "achieved": flop / sec / 1e12, "peak": fpeak, "unit": "TFLOP/s",
+            "frac": (flop / sec / 1e12 / fpeak) if fpeak else None,
+            "flop_per_decision": 2 * macs, "dims": dims,
+            "note": "dense-equivalent FLOPs of the Q-net forward over the RL cells' kernel time "
+                    "(the whole fused tick, not the forward alone; zero inputs are skipped)",
+            "peak_source": "measured DMUL+DADD (profiles/fp64_peak.json, tools/fp64_peak.cu)"}
     if len(cells) > 1:
         line["per_policy"] = {c["policy"]: {"decisions": int(st["ticks"].sum()),
                                             "kernel_ms": ms,

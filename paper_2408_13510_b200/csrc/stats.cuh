@@ -5,7 +5,8 @@
 //  * fp64 sums (E2E, TTFT, TBT, router wait): compute_metrics accumulates
 //    them sequentially in pool-index order, so warp 0 walks the replay in
 //    32-request chunks and adds the shuffled terms one by one in index order
-//    (bit-identical; a tree reduction would not be).
+//    (bit-identical; a tree reduction would not be), while warps 1..7 run
+//    the order-free reductions and the selections below.
 //  * counts, token / preemption totals, first arrival, last completion:
 //    order-free integer / min / max reductions over all threads.
 //  * nearest-rank p50/p90/p99 of E2E, TTFT, TBT (aggregate_of): no sort is
@@ -73,42 +74,56 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
     }
     __syncthreads();
     if (t < kWarp) {
-      // compute_metrics order (metrics.hpp:94-121): sequential pool-order sums
+      // compute_metrics order (metrics.hpp:94-121): sequential pool-order
+      // sums.  Blocks of 4 x 32 requests; the next block's loads are issued
+      // before the current block is summed (the add chain, not DRAM latency,
+      // bounds this loop).
       double se = 0.0, st = 0.0, sb = 0.0, sw = 0.0;
-      for (int b0 = 0; b0 < n; b0 += kWarp) {
-        const int j = b0 + lane;
-        const long long g = off + j;
-        const double comp = j < n ? P.completion[g] : -1.0;
-        const bool c = comp >= 0.0;
-        double e = 0.0, f = 0.0, tb = 0.0, w = 0.0;
-        bool htb = false, hw = false;
-        if (c) {
-          const double arr = P.arrival[g];
-          const double fst = P.first[g];
-          const double rt = P.routed[g];
-          const int d = P.decode[g];  // tokens_emitted at completion
-          e = __dsub_rn(comp, arr);
-          f = __dsub_rn(fst, arr);
-          if (d >= 2) {
-            htb = true;
-            tb = __ddiv_rn(__dsub_rn(comp, fst), (double)(d - 1));
-          }
-          if (rt >= 0.0) {
-            hw = true;
-            w = __dsub_rn(rt, arr);
-          }
+      constexpr int U = 4;
+      double cc[U], ca[U], cf[U], cr[U];
+      int cd[U];
+      auto load = [&](int b0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = b0 + u * kWarp + lane;
+          const long long g = off + j;
+          cc[u] = j < n ? P.completion[g] : -1.0;
+          ca[u] = j < n ? P.arrival[g] : 0.0;
+          cf[u] = j < n ? P.first[g] : 0.0;
+          cr[u] = j < n ? P.routed[g] : -1.0;
+          cd[u] = j < n ? P.decode[g] : 0;
         }
-        const unsigned cm = __ballot_sync(kFull, c), tm = __ballot_sync(kFull, htb),
-                       wm = __ballot_sync(kFull, hw);
-        for (int k = 0; k < kWarp; ++k) {
-          const double ek = __shfl_sync(kFull, e, k), fk = __shfl_sync(kFull, f, k);
-          const double bk = __shfl_sync(kFull, tb, k), wk = __shfl_sync(kFull, w, k);
-          if ((cm >> k) & 1u) {
-            se = __dadd_rn(se, ek);
-            st = __dadd_rn(st, fk);
+      };
+      if (n > 0) load(0);
+      for (int b0 = 0; b0 < n; b0 += U * kWarp) {
+        double e[U], f[U], tb[U], w[U];
+        unsigned cm[U], tm[U], wm[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const bool c = cc[u] >= 0.0;
+          const bool htb = c && cd[u] >= 2;
+          const bool hw = c && cr[u] >= 0.0;
+          e[u] = c ? __dsub_rn(cc[u], ca[u]) : 0.0;
+          f[u] = c ? __dsub_rn(cf[u], ca[u]) : 0.0;
+          tb[u] = htb ? __ddiv_rn(__dsub_rn(cc[u], cf[u]), (double)(cd[u] - 1)) : 0.0;
+          w[u] = hw ? __dsub_rn(cr[u], ca[u]) : 0.0;
+          cm[u] = __ballot_sync(kFull, c);
+          tm[u] = __ballot_sync(kFull, htb);
+          wm[u] = __ballot_sync(kFull, hw);
+        }
+        if (b0 + U * kWarp < n) load(b0 + U * kWarp);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          for (int k = 0; k < kWarp; ++k) {
+            const double ek = __shfl_sync(kFull, e[u], k), fk = __shfl_sync(kFull, f[u], k);
+            const double bk = __shfl_sync(kFull, tb[u], k), wk = __shfl_sync(kFull, w[u], k);
+            if ((cm[u] >> k) & 1u) {
+              se = __dadd_rn(se, ek);
+              st = __dadd_rn(st, fk);
+            }
+            if ((tm[u] >> k) & 1u) sb = __dadd_rn(sb, bk);
+            if ((wm[u] >> k) & 1u) sw = __dadd_rn(sw, wk);
           }
-          if ((tm >> k) & 1u) sb = __dadd_rn(sb, bk);
-          if ((wm >> k) & 1u) sw = __dadd_rn(sw, wk);
         }
       }
       if (t == 0) {
@@ -118,75 +133,93 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
         sums[3] = sw;
       }
     }
-    // order-free aggregates (every thread, warp 0 included)
-    int c_done = 0, c_tbt = 0;
-    long long pre = 0, tok = 0;
-    unsigned long long kmin = ~0ull, kmax = 0ull;
-    for (int i = t; i < n; i += kStatsThreads) {
-      const double comp = P.completion[off + i];
-      if (comp >= 0.0) {
-        const int d = P.decode[off + i];
-        c_done++;
-        c_tbt += d >= 2;
-        tok += d;
-        pre += P.preempt[off + i];
-        const unsigned long long ka = key_of(P.arrival[off + i]), kc = key_of(comp);
-        kmin = ka < kmin ? ka : kmin;
-        kmax = kc > kmax ? kc : kmax;
-      }
-    }
-    atomicAdd(&counts[0], c_done);
-    atomicAdd(&counts[1], c_tbt);
-    atomicAdd(&red_ll[0], (unsigned long long)pre);
-    atomicAdd(&red_ll[1], (unsigned long long)tok);
-    atomicMin(&red_key[0], kmin);
-    atomicMax(&red_key[1], kmax);
-    __syncthreads();
-    const int ne = counts[0], nt = counts[1];
-    if (t < kSel) {
-      const int metric = t / 3;
-      const double q = (t % 3) == 0 ? 0.50 : ((t % 3) == 1 ? 0.90 : 0.99);
-      const int cnt = metric == 2 ? nt : ne;
-      krem[t] = cnt > 0 ? nearest_rank_index(q, cnt) : -1;
-      prefix[t] = 0;
-    }
-    for (int pass = 0; pass < 8; ++pass) {
-      for (int k = t; k < kSel * 256; k += kStatsThreads) (&hist[0][0])[k] = 0;
-      __syncthreads();
-      const int sh = 56 - 8 * pass;
-      for (int i = t; i < n; i += kStatsThreads) {
+    else {
+      // warps 1..7, concurrently with warp 0's sums: order-free aggregates
+      // and the radix select (named barrier 1 over these 224 threads)
+      constexpr int NT = kStatsThreads - kWarp;
+      const int tt = t - kWarp;
+      auto bar = [] { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); };
+      int c_done = 0, c_tbt = 0;
+      long long pre = 0, tok = 0;
+      unsigned long long kmin = ~0ull, kmax = 0ull;
+      for (int i = tt; i < n; i += NT) {
         const double comp = P.completion[off + i];
-        if (!(comp >= 0.0)) continue;
-        const double arr = P.arrival[off + i];
-        const double fst = P.first[off + i];
-        const int d = P.decode[off + i];
-        unsigned long long key[3];
-        key[0] = key_of(__dsub_rn(comp, arr));
-        key[1] = key_of(__dsub_rn(fst, arr));
-        key[2] = d >= 2 ? key_of(__ddiv_rn(__dsub_rn(comp, fst), (double)(d - 1))) : 0ull;
+        if (comp >= 0.0) {
+          const int d = P.decode[off + i];
+          c_done++;
+          c_tbt += d >= 2;
+          tok += d;
+          pre += P.preempt[off + i];
+          const unsigned long long ka = key_of(P.arrival[off + i]), kc = key_of(comp);
+          kmin = ka < kmin ? ka : kmin;
+          kmax = kc > kmax ? kc : kmax;
+        }
+      }
+      atomicAdd(&counts[0], c_done);
+      atomicAdd(&counts[1], c_tbt);
+      atomicAdd(&red_ll[0], (unsigned long long)pre);
+      atomicAdd(&red_ll[1], (unsigned long long)tok);
+      atomicMin(&red_key[0], kmin);
+      atomicMax(&red_key[1], kmax);
+      bar();
+      if (tt < kSel) {
+        const int metric = tt / 3;
+        const double q = (tt % 3) == 0 ? 0.50 : ((tt % 3) == 1 ? 0.90 : 0.99);
+        const int cnt = metric == 2 ? counts[1] : counts[0];
+        krem[tt] = cnt > 0 ? nearest_rank_index(q, cnt) : -1;
+        prefix[tt] = 0;
+      }
+      for (int pass = 0; pass < 8; ++pass) {
+        for (int k = tt; k < kSel * 256; k += NT) (&hist[0][0])[k] = 0;
+        bar();
+        const int sh = 56 - 8 * pass;
+        constexpr int U = 4;  // 4 requests per thread per iteration: loads first
+        for (int i0 = tt; i0 < n; i0 += U * NT) {
+          double comp[U], arr[U], fst[U];
+          int d[U];
 #pragma unroll
-        for (int s = 0; s < kSel; ++s) {
-          const int mtr = s / 3;
-          if (mtr == 2 && d < 2) continue;
-          if (krem[s] < 0) continue;
-          const unsigned long long kk = key[mtr];
-          if (pass > 0 && (kk >> (sh + 8)) != prefix[s]) continue;
-          atomicAdd(&hist[s][(kk >> sh) & 0xffu], 1u);
+          for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * NT;
+            comp[u] = i < n ? P.completion[off + i] : -1.0;
+            arr[u] = i < n ? P.arrival[off + i] : 0.0;
+            fst[u] = i < n ? P.first[off + i] : 0.0;
+            d[u] = i < n ? P.decode[off + i] : 0;
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (!(comp[u] >= 0.0)) continue;
+            unsigned long long key[3];
+            key[0] = key_of(__dsub_rn(comp[u], arr[u]));
+            key[1] = key_of(__dsub_rn(fst[u], arr[u]));
+            key[2] = d[u] >= 2 ? key_of(__ddiv_rn(__dsub_rn(comp[u], fst[u]), (double)(d[u] - 1)))
+                               : 0ull;
+#pragma unroll
+            for (int s2 = 0; s2 < kSel; ++s2) {
+              const int mtr = s2 / 3;
+              if (mtr == 2 && d[u] < 2) continue;
+              if (krem[s2] < 0) continue;
+              const unsigned long long kk = key[mtr];
+              if (pass > 0 && (kk >> (sh + 8)) != prefix[s2]) continue;
+              atomicAdd(&hist[s2][(kk >> sh) & 0xffu], 1u);
+            }
+          }
         }
-      }
-      __syncthreads();
-      if (t < kSel && krem[t] >= 0) {  // bucket holding rank krem
-        int below = 0, dig = 0;
-        for (int b = 0; b < 256; ++b) {
-          const int h = (int)hist[t][b];
-          if (below + h > krem[t]) { dig = b; break; }
-          below += h;
+        bar();
+        if (tt < kSel && krem[tt] >= 0) {  // bucket holding rank krem
+          int below = 0, dig = 0;
+          for (int b = 0; b < 256; ++b) {
+            const int h = (int)hist[tt][b];
+            if (below + h > krem[tt]) { dig = b; break; }
+            below += h;
+          }
+          prefix[tt] = (prefix[tt] << 8) | (unsigned long long)dig;
+          krem[tt] -= below;
         }
-        prefix[t] = (prefix[t] << 8) | (unsigned long long)dig;
-        krem[t] -= below;
+        bar();
       }
-      __syncthreads();
     }
+    __syncthreads();  // join: sums (warp 0) + selections (warps 1..7)
+    const int ne = counts[0], nt = counts[1];
     if (t == 0) {
       rs_replay_stats& s = P.stats[r];
       double v[kSel];
