@@ -4,7 +4,7 @@
 //
 //  * fp64 sums (E2E, TTFT, TBT, router wait): compute_metrics accumulates
 //    them sequentially in pool-index order, so warp 0 walks the replay in
-//    32-request chunks and adds the shuffled terms one by one in index order
+//    128-request blocks and one lane adds the staged terms in index order
 //    (bit-identical; a tree reduction would not be), while warps 1..7 run
 //    the order-free reductions and the selections below.
 //  * counts, token / preemption totals, first arrival, last completion:
@@ -51,7 +51,7 @@ __device__ __forceinline__ int nearest_rank_index(double q, int n) {
   return (int)(idx < n - 1 ? idx : n - 1);
 }
 
-__global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_constant__ StatsParams P) {
+__global__ void __launch_bounds__(kStatsThreads, 3) stats_kernel(const __grid_constant__ StatsParams P) {
   __shared__ unsigned hist[kSel][256];
   __shared__ unsigned long long prefix[kSel];
   __shared__ int krem[kSel];
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
   __shared__ unsigned long long red_ll[2];      // total preemptions, total tokens
   __shared__ unsigned long long red_key[2];     // min key(arrival), max key(completion)
   __shared__ double sums[4];                    // e2e, ttft, tbt, router wait
+  __shared__ double stage[4][4 * kWarp];        // warp 0's staged sum terms
   const int t = threadIdx.x;
   const int lane = t & (kWarp - 1);
   for (int r = blockIdx.x; r < P.num_replays; r += gridDim.x) {
@@ -75,9 +76,11 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
     __syncthreads();
     if (t < kWarp) {
       // compute_metrics order (metrics.hpp:94-121): sequential pool-order
-      // sums.  Blocks of 4 x 32 requests; the next block's loads are issued
-      // before the current block is summed (the add chain, not DRAM latency,
-      // bounds this loop).
+      // sums.  Every term is >= +0 and the sums start at +0, so a skipped
+      // term (not completed, single-token TBT) is an exact +0.0 add.  Per
+      // block of 128 requests the lanes stage the four terms in shared
+      // memory and lane 0 runs the four add chains; the next block's global
+      // loads are in flight meanwhile.
       double se = 0.0, st = 0.0, sb = 0.0, sw = 0.0;
       constexpr int U = 4;
       double cc[U], ca[U], cf[U], cr[U];
@@ -96,35 +99,29 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
       };
       if (n > 0) load(0);
       for (int b0 = 0; b0 < n; b0 += U * kWarp) {
-        double e[U], f[U], tb[U], w[U];
-        unsigned cm[U], tm[U], wm[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const bool c = cc[u] >= 0.0;
-          const bool htb = c && cd[u] >= 2;
-          const bool hw = c && cr[u] >= 0.0;
-          e[u] = c ? __dsub_rn(cc[u], ca[u]) : 0.0;
-          f[u] = c ? __dsub_rn(cf[u], ca[u]) : 0.0;
-          tb[u] = htb ? __ddiv_rn(__dsub_rn(cc[u], cf[u]), (double)(cd[u] - 1)) : 0.0;
-          w[u] = hw ? __dsub_rn(cr[u], ca[u]) : 0.0;
-          cm[u] = __ballot_sync(kFull, c);
-          tm[u] = __ballot_sync(kFull, htb);
-          wm[u] = __ballot_sync(kFull, hw);
+          const int k = u * kWarp + lane;
+          stage[0][k] = c ? __dsub_rn(cc[u], ca[u]) : 0.0;
+          stage[1][k] = c ? __dsub_rn(cf[u], ca[u]) : 0.0;
+          stage[2][k] = c && cd[u] >= 2
+                            ? __ddiv_rn(__dsub_rn(cc[u], cf[u]), (double)(cd[u] - 1)) : 0.0;
+          stage[3][k] = c && cr[u] >= 0.0 ? __dsub_rn(cr[u], ca[u]) : 0.0;
         }
+        __syncwarp();
         if (b0 + U * kWarp < n) load(b0 + U * kWarp);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          for (int k = 0; k < kWarp; ++k) {
-            const double ek = __shfl_sync(kFull, e[u], k), fk = __shfl_sync(kFull, f[u], k);
-            const double bk = __shfl_sync(kFull, tb[u], k), wk = __shfl_sync(kFull, w[u], k);
-            if ((cm[u] >> k) & 1u) {
-              se = __dadd_rn(se, ek);
-              st = __dadd_rn(st, fk);
-            }
-            if ((tm[u] >> k) & 1u) sb = __dadd_rn(sb, bk);
-            if ((wm[u] >> k) & 1u) sw = __dadd_rn(sw, wk);
+        if (lane == 0) {
+          const int cnt = min(U * kWarp, n - b0);
+#pragma unroll 8
+          for (int k = 0; k < cnt; ++k) {
+            se = __dadd_rn(se, stage[0][k]);
+            st = __dadd_rn(st, stage[1][k]);
+            sb = __dadd_rn(sb, stage[2][k]);
+            sw = __dadd_rn(sw, stage[3][k]);
           }
         }
+        __syncwarp();
       }
       if (t == 0) {
         sums[0] = se;
@@ -173,7 +170,7 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
         for (int k = tt; k < kSel * 256; k += NT) (&hist[0][0])[k] = 0;
         bar();
         const int sh = 56 - 8 * pass;
-        constexpr int U = 4;  // 4 requests per thread per iteration: loads first
+        constexpr int U = 2;  // 2 requests per thread per iteration: loads first
         for (int i0 = tt; i0 < n; i0 += U * NT) {
           double comp[U], arr[U], fst[U];
           int d[U];
@@ -222,11 +219,10 @@ __global__ void __launch_bounds__(kStatsThreads) stats_kernel(const __grid_const
     const int ne = counts[0], nt = counts[1];
     if (t == 0) {
       rs_replay_stats& s = P.stats[r];
-      double v[kSel];
-      for (int k = 0; k < kSel; ++k) v[k] = krem[k] >= 0 ? value_of(prefix[k]) : 0.0;
-      s.e2e_p50 = v[0]; s.e2e_p90 = v[1]; s.e2e_p99 = v[2];
-      s.ttft_p50 = v[3]; s.ttft_p90 = v[4]; s.ttft_p99 = v[5];
-      s.tbt_p50 = v[6]; s.tbt_p90 = v[7]; s.tbt_p99 = v[8];
+      auto v = [&](int k) { return krem[k] >= 0 ? value_of(prefix[k]) : 0.0; };
+      s.e2e_p50 = v(0); s.e2e_p90 = v(1); s.e2e_p99 = v(2);
+      s.ttft_p50 = v(3); s.ttft_p90 = v(4); s.ttft_p99 = v(5);
+      s.tbt_p50 = v(6); s.tbt_p90 = v(7); s.tbt_p99 = v(8);
       s.percentiles_valid = 1;
       s.total_preemptions = (long long)red_ll[0];
       s.total_tokens = (long long)red_ll[1];
