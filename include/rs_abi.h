@@ -372,6 +372,55 @@ rs_status rs_generate_mixture_batch(const rs_profile* profile,
 rs_status rs_mlp_random_init(const int32_t* dims, int32_t num_layers, uint64_t seed,
                              double* params_out);
 
+/* ---- DQN training step ------------------------ */
+
+/* A sampled batch of transitions (Transition, replay.hpp:12-18), struct of
+ * arrays: state / next_state are [batch x state_dim] row-major. */
+typedef struct rs_dqn_batch {
+  int32_t batch;
+  int32_t _pad;
+  const double* state;
+  const int32_t* action;
+  const double* reward;
+  const double* next_state;
+  const uint8_t* done;
+} rs_dqn_batch;
+
+/* DqnAgent's trainable state: online / target networks (reference flat
+ * layout, as rs_batch_cfg.rl_params), AdamOptimizer moments and step count
+ * (mlp.hpp:159-189), updates_ and AgentConfig's learning rate / target sync
+ * interval (dqn.hpp:22-30).  Array pointers are device memory for
+ * rs_dqn_update, host memory for rs_dqn_update_host; the counters are
+ * advanced by the call. */
+typedef struct rs_dqn_state {
+  double* online;
+  double* target;
+  double* adam_m;
+  double* adam_v;
+  int64_t adam_t;                /* AdamOptimizer::t_ before the step */
+  int64_t updates;               /* DqnAgent::updates_ before the step */
+  int64_t target_sync_interval;  /* AgentConfig, default 1000 */
+  double learning_rate;          /* AgentConfig, default 1e-3 */
+} rs_dqn_state;
+
+/* Scratch bytes rs_dqn_update needs (per-sample activations and deltas). */
+rs_status rs_dqn_workspace_size(const rs_batch_cfg* cfg, int32_t batch, size_t* bytes);
+
+/* DqnAgent::update (dqn.hpp:107-127) after ReplayBuffer::sample: double-DQN
+ * targets (online argmax on s', target-net value, reward + discount * Q),
+ * Mlp::loss_and_gradient (mean Huber, mlp.hpp:78-136), AdamOptimizer::step
+ * (mlp.hpp:163-177), ++updates_ and sync_target every target_sync_interval
+ * updates — bit-identical to the reference.  Network shape from
+ * cfg->rl_num_layers / rl_dims.  *loss_out (device) receives the batch loss. */
+rs_status rs_dqn_update(const rs_batch_cfg* cfg, const rs_dqn_batch* batch, rs_dqn_state* state,
+                        double discount, double* loss_out, void* workspace,
+                        size_t workspace_bytes, void* cuda_stream);
+
+/* Same with host buffers (copied in and out every call) on `device`. */
+rs_status rs_dqn_update_host(const rs_batch_cfg* cfg, const rs_dqn_batch* batch,
+                             rs_dqn_state* state, double discount, double* loss_out,
+                             int32_t device);
+
 /* ---- host-side report layer (one replay) ------------------------------- */
 
 /* compute_metrics + emit_report (metrics.hpp:84-238) for one replay of a

@@ -519,6 +519,59 @@ int ref_emit_report(const rs_batch_cfg* cfg, int64_t n, const double* arrival,
   }
 }
 
+// `steps` DqnAgent::update calls (dqn.hpp:107-127) on a ReplayBuffer holding
+// the n given transitions, sampling with Rng(sample_seed) (replay.hpp:44-58).
+// The agent is DqnAgent(state_dim, actions, {hidden, lr, batch, sync}, 0) with
+// its online (and target) parameters replaced by params_in.  Per step: the
+// sampled transition indices (a copy of the Rng replays sample()'s draws),
+// the loss, and the online parameters after the step.
+int ref_dqn_train(int32_t state_dim, int32_t actions, int32_t hidden, const double* params_in,
+                  int64_t n, const double* states, const int32_t* acts, const double* rewards,
+                  const double* next_states, const uint8_t* dones, int32_t batch, int32_t steps,
+                  uint64_t sample_seed, double discount, double lr, int64_t sync_interval,
+                  int64_t* sampled_out, double* losses_out, double* online_out,
+                  double* target_out) {
+  try {
+    AgentConfig ac;
+    ac.hidden = hidden;
+    ac.learning_rate = lr;
+    ac.batch_size = static_cast<std::size_t>(batch);
+    ac.replay_capacity = static_cast<std::size_t>(std::max<int64_t>(n, batch));
+    ac.target_sync_interval = sync_interval;
+    DqnAgent agent(state_dim, actions, ac, 0);
+    auto& p = agent.online().params();
+    std::memcpy(p.data(), params_in, p.size() * sizeof(double));
+    agent.sync_target();
+    ReplayBuffer replay(static_cast<std::size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      Transition t;
+      t.state.assign(states + i * state_dim, states + (i + 1) * state_dim);
+      t.action = acts[i];
+      t.reward = rewards[i];
+      t.next_state.assign(next_states + i * state_dim, next_states + (i + 1) * state_dim);
+      t.done = dones[i] != 0;
+      replay.push(std::move(t));
+    }
+    Rng rng(sample_seed);
+    const std::size_t np = p.size();
+    for (int32_t k = 0; k < steps; ++k) {
+      Rng peek = rng;  // the draws update() is about to make
+      auto smp = replay.sample(static_cast<std::size_t>(batch), peek);
+      for (int32_t b = 0; b < batch; ++b)
+        sampled_out[static_cast<int64_t>(k) * batch + b] = smp[static_cast<std::size_t>(b)] - &replay.at(0);
+      auto loss = agent.update(replay, rng, discount);
+      losses_out[k] = loss ? *loss : -1.0;
+      std::memcpy(online_out + static_cast<std::size_t>(k) * np, agent.online().params().data(),
+                  np * sizeof(double));
+    }
+    std::memcpy(target_out, agent.target().params().data(), np * sizeof(double));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // CPU baseline: replays r in [0, R) of a CSR batch on `threads` host threads
 // (atomic work counter), outputs per replay stats only.  Returns wall seconds
 // (excluding nothing but thread start) or -1 on error.

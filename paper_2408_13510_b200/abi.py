@@ -194,6 +194,20 @@ class Trajectory(C.Structure):
                    (name, C.c_void_p) for name, _, _ in TRAJ_FIELDS]
 
 
+class DqnBatch(C.Structure):
+    """rs_dqn_batch: a sampled batch of transitions (replay.hpp:12-18)."""
+    _fields_ = [("batch", C.c_int32), ("_pad", C.c_int32), ("state", C.c_void_p),
+                ("action", C.c_void_p), ("reward", C.c_void_p), ("next_state", C.c_void_p),
+                ("done", C.c_void_p)]
+
+
+class DqnState(C.Structure):
+    """rs_dqn_state: online / target nets, Adam moments and counters."""
+    _fields_ = [("online", C.c_void_p), ("target", C.c_void_p), ("adam_m", C.c_void_p),
+                ("adam_v", C.c_void_p), ("adam_t", C.c_int64), ("updates", C.c_int64),
+                ("target_sync_interval", C.c_int64), ("learning_rate", C.c_double)]
+
+
 def make_trajectory(capacity: int, replays: int, m: int, r_w: float = 60.0,
                     gamma: float = 0.99, beta_d: float = 0.5, shaping: str = "guided",
                     episode_k: int = 0, fields=None):
@@ -329,6 +343,7 @@ EXPORTED_SYMBOLS = (
     "rs_generate_mixture", "rs_generate_mixture_batch", "rs_mix_seed",
     "rs_heavy_decode_cutoff", "rs_host_alloc", "rs_host_free", "rs_mlp_random_init",
     "rs_replay_trajectory", "rs_replay_trajectory_host", "rs_emit_report",
+    "rs_dqn_workspace_size", "rs_dqn_update", "rs_dqn_update_host",
 )
 
 
@@ -351,6 +366,11 @@ def _declare(lib: C.CDLL) -> None:
                                               P(Trajectory), C.c_int32]
     lib.rs_emit_report.argtypes = [C.c_char_p, P(BatchCfg), C.c_int64] + [C.c_void_p] * 10 + [
         P(Trajectory), C.c_int64]
+    lib.rs_dqn_workspace_size.argtypes = [P(BatchCfg), C.c_int32, P(C.c_size_t)]
+    lib.rs_dqn_update.argtypes = [P(BatchCfg), P(DqnBatch), P(DqnState), C.c_double, C.c_void_p,
+                                  C.c_void_p, C.c_size_t, C.c_void_p]
+    lib.rs_dqn_update_host.argtypes = [P(BatchCfg), P(DqnBatch), P(DqnState), C.c_double,
+                                       C.c_void_p, C.c_int32]
     lib.rs_mlp_forward_host.argtypes = [P(BatchCfg), C.c_void_p, C.c_int32, C.c_void_p,
                                         C.c_void_p, C.c_int32]
     lib.rs_generate_mixture.argtypes = [P(Profile), P(Thresholds), C.c_void_p, C.c_uint64,

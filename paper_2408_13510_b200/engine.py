@@ -12,6 +12,8 @@ Reference names are kept so harness code reads the same:
   record_trajectory + trajectory()               BatchSim.run_trajectory(policy, capacity,
     (env.hpp:131, 203, 305-319)                    reward, episode_k)
   RewardConfig (env.hpp:40-71)                   RewardConfig
+  DqnAgent::update (dqn.hpp:107-127) after      DqnTrainer.update(batch, discount)
+    ReplayBuffer::sample
   evaluate_policy over seeds                     BatchSim over the seed batch
     (experiment.hpp:648-670)
   build_workload (experiment.hpp:291-305)        build_workload(seed, n, rate, ...)
@@ -261,3 +263,44 @@ def mlp_random_init(dims, seed: int) -> np.ndarray:
     p = np.empty(abi.mlp_param_count(list(dims)), np.float64)
     abi.check(lib, lib.rs_mlp_random_init(d.ctypes.data, len(dims) - 1, int(seed), p.ctypes.data))
     return p
+
+
+class DqnTrainer:
+    """The trainable state of a DqnAgent (dqn.hpp:52-140) on the host: online
+    and target networks, Adam moments and counters.  `update` runs one
+    DqnAgent::update step on the device (rs_dqn_update_host) for a batch the
+    caller has sampled (ReplayBuffer::sample, replay.hpp:44-58)."""
+
+    def __init__(self, dims, params, learning_rate: float = 1e-3,
+                 target_sync_interval: int = 1000, device: int = 0):
+        self.dims = list(dims)
+        self.online = np.ascontiguousarray(params, dtype=np.float64).copy()
+        self.target = self.online.copy()
+        self.adam_m = np.zeros_like(self.online)
+        self.adam_v = np.zeros_like(self.online)
+        self.adam_t = 0
+        self.updates = 0
+        self.lr = float(learning_rate)
+        self.sync = int(target_sync_interval)
+        self.device = device
+        self.lib = abi.load_library()
+        self.cfg = abi.default_config("rl", max(1, self.dims[-1] - 1))
+        self.cfg.rl_num_layers = len(self.dims) - 1
+        for i, d in enumerate(self.dims):
+            self.cfg.rl_dims[i] = int(d)
+
+    def update(self, state, action, reward, next_state, done, discount: float) -> float:
+        c = lambda a, dt: np.ascontiguousarray(a, dtype=dt)
+        s, a, r = c(state, np.float64), c(action, np.int32), c(reward, np.float64)
+        ns, d = c(next_state, np.float64), c(done, np.uint8)
+        b = abi.DqnBatch(int(a.shape[0]), 0, s.ctypes.data, a.ctypes.data, r.ctypes.data,
+                         ns.ctypes.data, d.ctypes.data)
+        st = abi.DqnState(self.online.ctypes.data, self.target.ctypes.data,
+                          self.adam_m.ctypes.data, self.adam_v.ctypes.data, self.adam_t,
+                          self.updates, self.sync, self.lr)
+        loss = np.zeros(1, np.float64)
+        abi.check(self.lib, self.lib.rs_dqn_update_host(C.byref(self.cfg), C.byref(b),
+                                                        C.byref(st), float(discount),
+                                                        loss.ctypes.data, self.device))
+        self.adam_t, self.updates = int(st.adam_t), int(st.updates)
+        return float(loss[0])

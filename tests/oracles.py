@@ -307,3 +307,31 @@ def ref_emit_report(cfg, tr: Trace, directory, predictor_seed=1, policy_seed=0,
                              os.fsencode(str(directory)))
     if rc != 0:
         raise RuntimeError(ref_error())
+
+
+def ref_dqn_train(dims, params, states, actions, rewards, next_states, dones, batch, steps,
+                  sample_seed, discount, lr=1e-3, sync_interval=1000):
+    """`steps` reference DqnAgent::update calls; returns (sampled index
+    [steps, batch], losses [steps], online params after each step
+    [steps, np], final target params)."""
+    lib = ref_lib()
+    lib.ref_dqn_train.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64] + [
+        C.c_void_p] * 5 + [C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double, C.c_int64] + [
+        C.c_void_p] * 4
+    c = lambda a, dt: np.ascontiguousarray(a, dtype=dt)
+    params, states, next_states = c(params, np.float64), c(states, np.float64), c(next_states,
+                                                                                  np.float64)
+    actions, rewards, dones = c(actions, np.int32), c(rewards, np.float64), c(dones, np.uint8)
+    n, np_ = int(actions.shape[0]), int(params.shape[0])
+    idx = np.zeros((steps, batch), np.int64)
+    losses = np.zeros(steps, np.float64)
+    online = np.zeros((steps, np_), np.float64)
+    target = np.zeros(np_, np.float64)
+    rc = lib.ref_dqn_train(dims[0], dims[-1], dims[1], params.ctypes.data, n,
+                           states.ctypes.data, actions.ctypes.data, rewards.ctypes.data,
+                           next_states.ctypes.data, dones.ctypes.data, batch, steps, sample_seed,
+                           discount, lr, sync_interval, idx.ctypes.data, losses.ctypes.data,
+                           online.ctypes.data, target.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(ref_error())
+    return idx, losses, online, target
