@@ -42,3 +42,14 @@ def test_cpp_host_golden_run(exe, gpu):
     assert got["total_e2e_s"] == want["total_e2e_s"]
     assert got["makespan_s"] == want["makespan_s"]
     assert got["total_ttft_s"] / got["completed"] == want["ttft_s"]["mean"]
+
+
+@pytest.mark.gpu
+def test_cpp_host_report_and_dqn(exe, gpu, tmp_path):
+    """BatchSim::run_trajectory + emit_report (C++ mirror) write the reference's
+    golden summary.json byte for byte; DqnTrainer::update runs."""
+    r = subprocess.run([str(exe), str(tmp_path)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert (tmp_path / "summary.json").read_bytes() == GOLDEN.read_bytes()
+    assert (tmp_path / "timeseries.csv").read_text().startswith(
+        "tick,time_s,action,reward,router_queue,inst0_waiting")
