@@ -388,9 +388,10 @@ enum FastRun { kDone = 0, kRerunSeq = 1, kRerunInit = 2 };
 // ends unfinished (livelock, max_ticks, errors: rare) is re-run with init.
 // `seq` steps instances one at a time in index order (exact stop point of a
 // "nothing admissible" error).
-template <int POL, int G, int W>
+template <int POL, int G, int W, bool SEQ>
 __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const MlpView& M, int r,
-                                   bool seq, bool init, const Lanes<W>& L) {
+                                   bool init, const Lanes<W>& L) {
+  constexpr bool seq = SEQ;  // compile-time: the index-order re-run is a separate instantiation
   const int l = L.l;
   Replay R;
   R.off = P.offsets[r];
@@ -492,7 +493,12 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
     }
     const int action = decide_fast<POL, G, W>(P, gw, M, R, S, has_head, hr, hb, gbase, L);
     R.hash = hash_action(R.hash, action);
-    if (action < 0 || action > m) { R.status = RS_REPLAY_BAD_ACTION; break; }
+    // env.hpp:252-254: only an agent can produce an out-of-range action (the
+    // heuristics return 0..m by construction)
+    if (POL == RS_POLICY_RL && (action < 0 || action > m)) {
+      R.status = RS_REPLAY_BAD_ACTION;
+      break;
+    }
     const double t1 = __dadd_rn(R.clock, P.delta_t);
     int wdelta = 0;  // this lane's waiting-count change over the tick
     if (action < m && has_head) {
@@ -538,7 +544,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
     }
     unsigned fl = L.any(again) ? 2u : 0u;
     while (fl & 2u) {
-      if (seq) {  // only the lowest-index instance that still has work
+      if (SEQ) {  // only the lowest-index instance that still has work
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const int i = g * W + l;
@@ -719,8 +725,9 @@ __global__ void __launch_bounds__(256) replay_fast_kernel(const __grid_constant_
     if (L.l == 0) r = atomicAdd(P.work_counter, 1);
     r = L.shfl(r, 0);
     if (r >= P.num_replays) break;
-    const FastRun o = run_replay_fast<POL, G, W>(P, gw, gbase, M, r, false, false, L);
-    if (o != kDone) run_replay_fast<POL, G, W>(P, gw, gbase, M, r, o == kRerunSeq, true, L);
+    const FastRun o = run_replay_fast<POL, G, W, false>(P, gw, gbase, M, r, false, L);
+    if (o == kRerunSeq) run_replay_fast<POL, G, W, true>(P, gw, gbase, M, r, true, L);
+    else if (o == kRerunInit) run_replay_fast<POL, G, W, false>(P, gw, gbase, M, r, true, L);
   }
 }
 
