@@ -101,10 +101,12 @@ Layout make_layout(const rs_batch_cfg& c, int wcap, bool fast) {
   if (rl) {
     for (int l = 1; l < c.rl_num_layers; ++l) L.maxw = std::max(L.maxw, c.rl_dims[l]);
     L.maxw = std::max(L.maxw, 1);
-    // x, h0, h1, then the nonzero-input list (values, then int row offsets)
+    // x, h0, h1 (each rounded up to an even number of doubles), then the
+    // nonzero-input list of 16-byte {value, row} records
     const size_t lmax = (size_t)std::max(c.rl_dims[0], L.maxw);
-    off = align_up(off + (size_t)(c.rl_dims[0] + 2 * L.maxw + lmax) * sizeof(double) +
-                       lmax * sizeof(int), 16);
+    const size_t ev = ((size_t)c.rl_dims[0] + 1) & ~(size_t)1;
+    const size_t mw = ((size_t)L.maxw + 1) & ~(size_t)1;
+    off = align_up(off + (ev + 2 * mw + 2 * lmax) * sizeof(double), 16);
   }
   L.off_rng = (int)off;
   if (rl && c.rl_epsilon > 0.0) off = align_up(off + 312 * sizeof(unsigned long long), 16);

@@ -185,11 +185,13 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
       }
     }
     if (!P.rl_wt_global) {  // staged weights: LDS-only forward over nonzero inputs
+      // x | h0 | h1 | nonzero list, each region an even number of doubles
+      // (16-byte aligned: the list records and the paired weights load as
+      // 16-byte vectors)
       const int xd = (gw >> 1) + (P.off_rlx >> 3);
-      const int h0d = xd + P.rl_dims[0], h1d = h0d + P.rl_maxw, lvd = h1d + P.rl_maxw;
-      const int lmax = P.rl_dims[0] > P.rl_maxw ? P.rl_dims[0] : P.rl_maxw;
-      return mlp_forward_list(P.rl_dims, P.rl_woff, P.rl_boff, P.rl_layers, xd, h0d, h1d, lvd,
-                              (lvd + lmax) * 2, L);
+      const int mw = (P.rl_maxw + 1) & ~1;
+      const int h0d = xd + ((P.rl_dims[0] + 1) & ~1), h1d = h0d + mw, lvd = h1d + mw;
+      return mlp_forward_list(P.rl_dims, P.rl_woff, P.rl_boff, P.rl_layers, xd, h0d, h1d, lvd, L);
     }
     double* h0 = x + M.dims[0];
     double* h1 = h0 + P.rl_maxw;
