@@ -786,23 +786,32 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   rs_status s2 = launch_kernel(pl.kern, kp, pl.wpb, rs::kWarp / pl.width, pl.block_smem,
                                tr->num_replays, st);
   if (s2 != RS_OK) return s2;
-  // compute_metrics aggregates (metrics.hpp:62-162), one CTA per replay
-  if (inputs_done) RS_CUDA(cudaStreamWaitEvent(st, (cudaEvent_t)inputs_done, 0));
+  // compute_metrics aggregates (metrics.hpp:62-162), one CTA per replay;
+  // the streamed-input caller launches them itself once its copies are queued
+  if (inputs_done == kDeferStats) return RS_OK;
+  return rs_internal_stats(tr, out, stats, stream, inputs_done);
+}
+
+rs_status rs_internal_stats(const rs_trace_soa* tr, const rs_req_out* out, rs_replay_stats* stats,
+                            void* stream, void* wait_event) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (wait_event) RS_CUDA(cudaStreamWaitEvent(st, (cudaEvent_t)wait_event, 0));
   rs::StatsParams sp;
   sp.num_replays = tr->num_replays;
-  sp.offsets = kp.offsets;
-  sp.arrival = kp.arrival;
-  sp.decode = kp.decode;
-  sp.routed = kp.o_routed;
-  sp.first = kp.o_first;
-  sp.completion = kp.o_completion;
-  sp.preempt = kp.o_preempt;
+  sp.offsets = reinterpret_cast<const long long*>(tr->offsets);
+  sp.arrival = tr->arrival_s;
+  sp.decode = tr->decode_tokens;
+  sp.routed = out->routed_s;
+  sp.first = out->first_token_s;
+  sp.completion = out->completion_s;
+  sp.preempt = out->preemptions;
   sp.stats = stats;
-  {
-    const int grid = std::max(1, std::min(tr->num_replays, sms * 8));
-    rs::stats_kernel<<<grid, rs::kStatsThreads, 0, st>>>(sp);
-    RS_CUDA(cudaGetLastError());
-  }
+  int dev = 0, sms = 0;
+  RS_CUDA(cudaGetDevice(&dev));
+  RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int grid = std::max(1, std::min(tr->num_replays, sms * 8));
+  rs::stats_kernel<<<grid, rs::kStatsThreads, 0, st>>>(sp);
+  RS_CUDA(cudaGetLastError());
   return RS_OK;
 }
 

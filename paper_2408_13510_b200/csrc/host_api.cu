@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -196,6 +198,15 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
   char* b = nullptr;
   cudaStream_t st = nullptr;
   if ((s = arena(device, o, &b, &st)) != RS_OK) return s;
+  // RS_DEBUG_TIMING=1: per-call phase times on stderr (device events on the
+  // replay stream + host wall clock) — diagnosing e2e variance
+  const bool dbg = getenv("RS_DEBUG_TIMING") != nullptr;
+  const auto w0 = std::chrono::steady_clock::now();
+  cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
+  if (dbg) {
+    for (auto& e : tev) cudaEventCreate(&e);
+    cudaEventRecord(tev[0], st);
+  }
   auto h2d = [&](size_t off, const void* src, size_t n) -> cudaError_t {
     if (!src || n == 0) return cudaSuccess;
     return cudaMemcpyAsync(b + off, src, n, cudaMemcpyHostToDevice, st);
@@ -285,8 +296,13 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
     RS_CUDA2(cudaEventRecord(dc.ev_ready, st));
     const cudaStream_t cs = dc.copy_stream;
     RS_CUDA2(cudaStreamWaitEvent(cs, dc.ev_ready, 0));
-    // the copy stream is queued first (it only waits for the flag reset);
-    // the replay kernel then runs concurrently with it
+    // The replay kernel is launched FIRST: it starts at once and gates each
+    // 32-request window on the watermark, so the host-side cost of queueing
+    // the chunk copies (and any host hiccup meanwhile) overlaps the replay
+    // instead of delaying its launch.  The stats pass waits for the copies.
+    s = forward(rs_internal_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st, flag,
+                                         kDeferStats, nullptr));
+    if (s != RS_OK) return s;
     struct Col { size_t off; const void* src; size_t es; };
     const Col cols[4] = {{o_arr, tr->arrival_s, 8}, {o_pr, tr->prompt_tokens, 4},
                          {o_de, tr->decode_tokens, 4}, {o_tk, tr->task, 1}};
@@ -305,13 +321,14 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
       lo = hi;
     }
     RS_CUDA2(cudaEventRecord(dc.ev_done, cs));
-    s = forward(rs_internal_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st, flag,
-                                         dc.ev_done, nullptr));
+    s = forward(rs_internal_stats(&dt, &dout, dstats, st, dc.ev_done));
     if (s != RS_OK) {
       cudaStreamSynchronize(cs);
       return s;
     }
   }
+  if (dbg) cudaEventRecord(tev[1], st);
+  const auto w1 = std::chrono::steady_clock::now();
   auto d2h = [&](void* dst, size_t off, size_t n) -> cudaError_t {
     if (!dst || n == 0) return cudaSuccess;
     return cudaMemcpyAsync(dst, b + off, n, cudaMemcpyDeviceToHost, st);
@@ -328,7 +345,19 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
   for (int k = 0; htraj && k < 12; ++k)
     if (tf[k].host)
       RS_CUDA2(d2h(const_cast<void*>(tf[k].host), tf[k].off, tf[k].es * tf[k].mult * (size_t)nrec));
+  if (dbg) cudaEventRecord(tev[2], st);
   RS_CUDA2(cudaStreamSynchronize(st));
+  if (dbg) {
+    const auto w2 = std::chrono::steady_clock::now();
+    float a = 0.f, c = 0.f;
+    cudaEventElapsedTime(&a, tev[0], tev[1]);
+    cudaEventElapsedTime(&c, tev[1], tev[2]);
+    const auto ms = [](auto x, auto y) { return std::chrono::duration<double, std::milli>(y - x).count(); };
+    std::fprintf(stderr, "rs timing: device start->kernels done %.2f ms, d2h %.2f ms | host enqueue %.2f ms, "
+                 "wait %.2f ms, total %.2f ms (streamed %d)\n", a, c, ms(w0, w1), ms(w1, w2), ms(w0, w2),
+                 (int)stream_in);
+    for (auto& e : tev) cudaEventDestroy(e);
+  }
   // The reference leaves predicted_bucket unset (-1) for requests that never
   // reached the router queue; report those as 255.
   if (out && out->predicted_bucket) {
