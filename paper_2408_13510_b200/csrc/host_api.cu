@@ -273,9 +273,11 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
         RS_OK)
       return s;
   } else {
-    // chunk boundaries: small first chunk (the kernel starts on it), doubling
+    // chunk boundaries: a small first chunk (the kernel starts on it), then
+    // x8 (each chunk lands well before the replays consume the previous one;
+    // few chunks = few 2D copy commands to queue)
     std::vector<int> bounds;
-    for (int64_t e = std::min<int64_t>(n_eq, 128); ; e = std::min<int64_t>(n_eq, 2 * e)) {
+    for (int64_t e = std::min<int64_t>(n_eq, 256); ; e = std::min<int64_t>(n_eq, 8 * e)) {
       bounds.push_back((int)e);
       if (e == n_eq) break;
     }
