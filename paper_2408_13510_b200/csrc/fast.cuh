@@ -48,6 +48,11 @@ struct Inst {  // one instance, held in its lane's registers
   // waiting-queue aggregates in 32 bits: run_replay_fast refuses replays
   // whose N x max(prompt + max(decode, bucket bound)) could reach 2^31
   int resw, pendw, dlw, tlw, tokw;
+  // RL state encoding (encode_state, env.hpp:88-113) with the default state
+  // scheme {0, e1, e2}: running entries with decode_left >= e1 / >= e2, and
+  // the decode-step count D at which the next of them drops below e1 / e2
+  // (decode_left falls by one per decode step).  Exact between events.
+  int sb1, sb2, nx1, nx2;
 };
 
 // running entry fields (admission order) and waiting ring fields
@@ -93,6 +98,21 @@ __device__ __forceinline__ void inst_init(Inst& I) {
   I.o_head = I.o_tail = (int)kNil;
   I.comps = 0;
   I.resw = I.pendw = I.dlw = I.tlw = I.tokw = 0;
+  I.sb1 = I.sb2 = 0;
+  I.nx1 = I.nx2 = kBig;
+}
+
+// state-bucket tracking of one running entry with decode_left dl at step D
+__device__ __forceinline__ void sb_add(const KParams& P, Inst& I, int dl) {
+  const int e1 = P.state_edges[1], e2 = P.state_edges[2];
+  if (dl >= e1) {
+    I.sb1++;
+    I.nx1 = min(I.nx1, I.D + dl - e1 + 1);
+  }
+  if (dl >= e2) {
+    I.sb2++;
+    I.nx2 = min(I.nx2, I.D + dl - e2 + 1);
+  }
 }
 
 __device__ __forceinline__ void waitagg(Inst& I, int prompt, int dhat, int tru, int emit, int s) {
@@ -209,6 +229,7 @@ __device__ __forceinline__ void lane_admit_one(const KParams& P, int gw, int i, 
   else I.next_ge = ge_at < I.next_ge ? ge_at : I.next_ge;
   const int done_at = tru - emit + I.D;
   I.next_done = done_at < I.next_done ? done_at : I.next_done;
+  sb_add(P, I, dhat - emit);
   waitagg(I, prompt, dhat, tru, emit, -1);
 }
 
@@ -282,7 +303,8 @@ __device__ inline void lane_admit(const KParams& P, int gw, long long off, int i
 // A whole warp keeps its <= 4 entries per lane in registers; a narrower
 // group streams the batch in W-entry chunks, compacting as it goes (an
 // entry only ever moves down, onto a slot already read).
-template <int W>
+// SB: also recount the RL state-bucket tracking (Inst::sb1..nx2).
+template <int W, bool SB>
 __device__ inline void warp_scan_instance(const KParams& P, int gw, long long off, int i,
                                           int owner, Inst& I, const Lanes<W>& L) {
   const int l = L.l;
@@ -290,6 +312,7 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
   const int n = L.shfl(I.n, owner);
   const double clock = L.shfl(I.clock, owner);
   int res = 0, kv = 0, dl = 0, tl = 0, tok = 0, nge = 0, nxg = kBig, nxd = kBig;
+  int s1 = 0, s2 = 0, x1 = kBig, x2 = kBig;
   int ncomp = 0;
   auto account = [&](int pr, int dh, int tr, int ky) {
     const int em = D + ky;
@@ -302,6 +325,11 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
     if (em >= dh) nge++;
     else nxg = min(nxg, dh - ky);
     nxd = min(nxd, tr - ky);
+    if (SB) {
+      const int e1 = P.state_edges[1], e2 = P.state_edges[2];
+      if (d >= e1) { s1++; x1 = min(x1, D + d - e1 + 1); }
+      if (d >= e2) { s2++; x2 = min(x2, D + d - e2 + 1); }
+    }
   };
   if (W == kWarp) {
     int rq[kMaxRunChunks], pr[kMaxRunChunks], dh[kMaxRunChunks], tr[kMaxRunChunks],
@@ -388,8 +416,20 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
   nge = L.sum(nge);
   nxg = L.min(nxg);
   nxd = L.min(nxd);
+  if (SB) {
+    s1 = L.sum(s1);
+    s2 = L.sum(s2);
+    x1 = L.min(x1);
+    x2 = L.min(x2);
+  }
   L.sync();
   if (l == owner) {
+    if (SB) {
+      I.sb1 = s1;
+      I.sb2 = s2;
+      I.nx1 = x1;
+      I.nx2 = x2;
+    }
     I.n = n - ncomp;
     I.comps += ncomp;
     I.res = res;
@@ -410,6 +450,8 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
 // No request can complete here: completions were handled this step.
 __device__ inline void lane_recount(const KParams& P, int gw, int i, Inst& I) {
   int res = 0, kv = 0, dl = 0, tl = 0, tok = 0, nge = 0, nxg = kBig, nxd = kBig;
+  I.sb1 = I.sb2 = 0;
+  I.nx1 = I.nx2 = kBig;
   for (int j = 0; j < I.n; ++j) {
     const int pr = RP(P, gw, i, j), dh = RD(P, gw, i, j), tr = RT(P, gw, i, j),
               ky = RK(P, gw, i, j);
@@ -422,6 +464,7 @@ __device__ inline void lane_recount(const KParams& P, int gw, int i, Inst& I) {
     if (em >= dh) nge++;
     else nxg = min(nxg, dh - ky);
     nxd = min(nxd, tr - ky);
+    sb_add(P, I, dh - em);
   }
   I.res = res;
   I.kv = kv;

@@ -63,7 +63,7 @@ __device__ __forceinline__ int grp_argmax_key(const Lanes<W>& L, unsigned long l
 
 template <int POL, int G, int W>
 __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Replay& R,
-                                  const Inst (&S)[G], bool has_head, const Rec& hr, int hb,
+                                  Inst (&S)[G], bool has_head, const Rec& hr, int hb,
                                   char* gbase, const Lanes<W>& L) {
   const int l = L.l;
   const int m = P.m;
@@ -136,16 +136,18 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
         int cge[RS_MAX_BUCKETS + 1];
 #pragma unroll
         for (int b = 0; b < RS_MAX_BUCKETS; ++b) cge[b] = 0;
-        if (nsb == 3) {  // BucketScheme::state_default {0, 256, 2048}
-          const int e1 = P.state_edges[1], e2 = P.state_edges[2];
-          int c1 = 0, c2 = 0;
-          for (int j = 0; j < S[g].n; ++j) {
-            const int d = RD(P, gw, i, j) - (S[g].D + RK(P, gw, i, j));
-            c1 += d >= e1;
-            c2 += d >= e2;
+        if (nsb == 3) {  // three state edges {0, e1, e2} (BucketScheme::state_default)
+          // tracked counts, exact until decode_left of a tracked entry drops
+          // below an edge (D reaches nx1 / nx2): then recount the batch
+          Inst& I = S[g];
+          if (I.D >= I.nx1 || I.D >= I.nx2) {
+            I.sb1 = I.sb2 = 0;
+            I.nx1 = I.nx2 = kBig;
+            for (int j = 0; j < I.n; ++j)
+              sb_add(P, I, RD(P, gw, i, j) - (I.D + RK(P, gw, i, j)));
           }
-          cge[1] = c1;
-          cge[2] = c2;
+          cge[1] = I.sb1;
+          cge[2] = I.sb2;
         } else {
           for (int j = 0; j < S[g].n; ++j) {
             int d = RD(P, gw, i, j) - (S[g].D + RK(P, gw, i, j));
@@ -657,7 +659,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
         while (sm) {
           const int owner = __ffs(sm) - 1;
           sm &= sm - 1;
-          warp_scan_instance(P, gw, off, g * W + owner, owner, S[g], L);
+          warp_scan_instance<W, POL == RS_POLICY_RL>(P, gw, off, g * W + owner, owner, S[g], L);
         }
         if (mine && S[g].kv > P.kv_cap && S[g].n > 1) {
           const int w0 = S[g].w_cnt + S[g].o_cnt;
