@@ -519,7 +519,8 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     const int target = std::min<long long>(16, ((long long)tr->num_replays + sms0 - 1) / sms0);
     auto per_sm = [&](const Layout& Lx) {
       int best = 0;
-      for (int wpb = 1; wpb <= 8; ++wpb) {
+      const int wmax = cfg->policy == RS_POLICY_RL ? 16 : 8;
+      for (int wpb = 1; wpb <= wmax; ++wpb) {
         const long long bytes = (long long)Lx.weights_bytes + (long long)wpb * Lx.group_bytes;
         const int blocks = std::min<long long>(32 / wpb, (228 * 1024) / (bytes + 1024));
         best = std::max(best, blocks * wpb);
@@ -712,7 +713,9 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     pl.kern = kernel_for(cfg->policy, fast, groups, width);
     if (!pl.kern) return pl;
     const int gpw = rs::kWarp / width;
-    for (int wpb = 8; wpb >= 1; --wpb) {
+    // the fast RL kernel is compiled for blocks of up to 16 warps
+    const int max_wpb = (fast && cfg->policy == RS_POLICY_RL) ? 16 : 8;
+    for (int wpb = max_wpb; wpb >= 1; --wpb) {
       if (wpb_env && wpb != wpb_env) continue;
       const long long bytes = L.weights_bytes + (long long)wpb * gpw * L.group_bytes;
       if (bytes > smem_optin) continue;

@@ -699,8 +699,14 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
   return kDone;
 }
 
+// Up to 8 replay warps per block; the RL kernel up to 16: its Q-network is
+// staged once per block, so one wide block per SM leaves the most shared
+// memory for replay slots (512 threads x 128 registers = the register file).
+template <int POL>
+constexpr int fast_max_threads() { return POL == RS_POLICY_RL ? 512 : 256; }
+
 template <int POL, int G, int W>
-__global__ void __launch_bounds__(256) replay_fast_kernel(const __grid_constant__ KParams P) {
+__global__ void __launch_bounds__(fast_max_threads<POL>()) replay_fast_kernel(const __grid_constant__ KParams P) {
   extern __shared__ __align__(16) char smem[];
   const Lanes<W> L = make_lanes<W>();
   MlpView M;
