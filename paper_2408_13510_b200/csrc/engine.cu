@@ -717,6 +717,10 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     const int max_wpb = (fast && cfg->policy == RS_POLICY_RL) ? 16 : 8;
     for (int wpb = max_wpb; wpb >= 1; --wpb) {
       if (wpb_env && wpb != wpb_env) continue;
+      // wide RL blocks only in whole multiples of the 4 SM sub-partitions:
+      // 9 warps would put 3 replays on one scheduler and 2 on the others,
+      // and the slowest scheduler's replays set the tail (measured on c3)
+      if (wpb > 8 && (wpb & 3)) continue;
       const long long bytes = L.weights_bytes + (long long)wpb * gpw * L.group_bytes;
       if (bytes > smem_optin) continue;
       if (cudaFuncSetAttribute(pl.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
