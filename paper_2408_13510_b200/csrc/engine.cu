@@ -273,30 +273,30 @@ using KernelFn = void (*)(rs::KParams);
 // parallel) instantiates that policy's general and fast replay kernels.
 namespace rs {
 using KernelFn = void (*)(KParams);
-KernelFn kernel_for_0(bool fast, int groups, int width);
-KernelFn kernel_for_1(bool fast, int groups, int width);
-KernelFn kernel_for_2(bool fast, int groups, int width);
-KernelFn kernel_for_3(bool fast, int groups, int width);
-KernelFn kernel_for_4(bool fast, int groups, int width);
-KernelFn kernel_for_5(bool fast, int groups, int width);
-KernelFn kernel_for_6(bool fast, int groups, int width);
-KernelFn kernel_for_7(bool fast, int groups, int width);
-KernelFn kernel_for_8(bool fast, int groups, int width);
+KernelFn kernel_for_0(bool fast, int groups, int width, bool wide);
+KernelFn kernel_for_1(bool fast, int groups, int width, bool wide);
+KernelFn kernel_for_2(bool fast, int groups, int width, bool wide);
+KernelFn kernel_for_3(bool fast, int groups, int width, bool wide);
+KernelFn kernel_for_4(bool fast, int groups, int width, bool wide);
+KernelFn kernel_for_5(bool fast, int groups, int width, bool wide);
+KernelFn kernel_for_6(bool fast, int groups, int width, bool wide);
+KernelFn kernel_for_7(bool fast, int groups, int width, bool wide);
+KernelFn kernel_for_8(bool fast, int groups, int width, bool wide);
 }  // namespace rs
 
 namespace {
 
-KernelFn kernel_for(int policy, bool fast, int groups, int width) {
+KernelFn kernel_for(int policy, bool fast, int groups, int width, bool wide = false) {
   switch (policy) {
-    case 0: return rs::kernel_for_0(fast, groups, width);
-    case 1: return rs::kernel_for_1(fast, groups, width);
-    case 2: return rs::kernel_for_2(fast, groups, width);
-    case 3: return rs::kernel_for_3(fast, groups, width);
-    case 4: return rs::kernel_for_4(fast, groups, width);
-    case 5: return rs::kernel_for_5(fast, groups, width);
-    case 6: return rs::kernel_for_6(fast, groups, width);
-    case 7: return rs::kernel_for_7(fast, groups, width);
-    case 8: return rs::kernel_for_8(fast, groups, width);
+    case 0: return rs::kernel_for_0(fast, groups, width, wide);
+    case 1: return rs::kernel_for_1(fast, groups, width, wide);
+    case 2: return rs::kernel_for_2(fast, groups, width, wide);
+    case 3: return rs::kernel_for_3(fast, groups, width, wide);
+    case 4: return rs::kernel_for_4(fast, groups, width, wide);
+    case 5: return rs::kernel_for_5(fast, groups, width, wide);
+    case 6: return rs::kernel_for_6(fast, groups, width, wide);
+    case 7: return rs::kernel_for_7(fast, groups, width, wide);
+    case 8: return rs::kernel_for_8(fast, groups, width, wide);
   }
   return nullptr;
 }
@@ -712,9 +712,11 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     pl.width = width;
     pl.kern = kernel_for(cfg->policy, fast, groups, width);
     if (!pl.kern) return pl;
+    KernelFn wide = kernel_for(cfg->policy, fast, groups, width, true);
     const int gpw = rs::kWarp / width;
-    // the fast RL kernel is compiled for blocks of up to 16 warps
-    const int max_wpb = (fast && cfg->policy == RS_POLICY_RL) ? 16 : 8;
+    // the wide RL instantiation takes blocks of up to 16 warps
+    const int max_wpb = wide ? 16 : 8;
+    KernelFn narrow = pl.kern;
     for (int wpb = max_wpb; wpb >= 1; --wpb) {
       if (wpb_env && wpb != wpb_env) continue;
       // wide RL blocks only in whole multiples of the 4 SM sub-partitions:
@@ -723,13 +725,14 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
       if (wpb > 8 && (wpb & 3)) continue;
       const long long bytes = L.weights_bytes + (long long)wpb * gpw * L.group_bytes;
       if (bytes > smem_optin) continue;
-      if (cudaFuncSetAttribute(pl.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      KernelFn k = wpb > 8 ? wide : narrow;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
           cudaSuccess) {
         cudaGetLastError();
         continue;
       }
       int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pl.kern, wpb * rs::kWarp,
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, wpb * rs::kWarp,
                                                         (size_t)bytes) != cudaSuccess) {
         cudaGetLastError();
         continue;
@@ -737,6 +740,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
       per_sm = std::min(per_sm, (int)(smem_sm / (bytes + 1024)));
       const long long cap = (long long)sms * per_sm * wpb * gpw;
       if (cap > pl.capacity) {
+        pl.kern = k;
         pl.capacity = cap;
         pl.wpb = wpb;
         pl.per_sm = per_sm;
@@ -778,6 +782,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
         if (L.weights_bytes + wpb * L.group_bytes <= smem_optin) {
           pl.wpb = wpb;
           pl.block_smem = L.weights_bytes + wpb * L.group_bytes;
+          pl.kern = kernel_for(cfg->policy, fast, groups, pl.width);  // <= 8 warps
           break;
         }
       }

@@ -699,14 +699,8 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
   return kDone;
 }
 
-// Up to 8 replay warps per block; the RL kernel up to 16: its Q-network is
-// staged once per block, so one wide block per SM leaves the most shared
-// memory for replay slots (512 threads x 128 registers = the register file).
-template <int POL>
-constexpr int fast_max_threads() { return POL == RS_POLICY_RL ? 512 : 256; }
-
 template <int POL, int G, int W>
-__global__ void __launch_bounds__(fast_max_threads<POL>()) replay_fast_kernel(const __grid_constant__ KParams P) {
+__device__ __forceinline__ void replay_fast_body(const KParams& P) {
   extern __shared__ __align__(16) char smem[];
   const Lanes<W> L = make_lanes<W>();
   MlpView M;
@@ -739,6 +733,22 @@ __global__ void __launch_bounds__(fast_max_threads<POL>()) replay_fast_kernel(co
     if (o == kRerunSeq) run_replay_fast<POL, G, W, true>(P, gw, gbase, M, r, true, L);
     else if (o == kRerunInit) run_replay_fast<POL, G, W, false>(P, gw, gbase, M, r, true, L);
   }
+}
+
+// Up to 8 replay warps per block.
+template <int POL, int G, int W>
+__global__ void __launch_bounds__(256) replay_fast_kernel(const __grid_constant__ KParams P) {
+  replay_fast_body<POL, G, W>(P);
+}
+
+// Up to 16 (the RL policy in the throughput regime): its Q-network is staged
+// once per block, so one wide block per SM leaves the most shared memory for
+// replay slots (512 threads x 128 registers = the register file).  A separate
+// instantiation: the 512-thread bound changes the code ptxas generates, and
+// blocks of <= 8 warps run faster with the 256-thread build (measured, c3).
+template <int POL, int G, int W>
+__global__ void __launch_bounds__(512) replay_fast_kernel_wide(const __grid_constant__ KParams P) {
+  replay_fast_body<POL, G, W>(P);
 }
 
 }  // namespace rs
