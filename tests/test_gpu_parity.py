@@ -114,10 +114,14 @@ def test_batched_replays_match_oracle(gpu, pol):
 
 
 @pytest.mark.parametrize("m,eps,glob", [(4, 0.0, 0), (8, 0.0, 0), (4, 0.3, 0), (2, 0.0, 0),
-                                        (8, 0.0, 1), (64, 0.0, 0)])
+                                        (8, 0.0, 1), (64, 0.0, 0), (4, 0.0, "wide"),
+                                        (4, 0.3, "wide")])
 def test_rl_router_matches_oracle(gpu, m, eps, glob, monkeypatch):
-    # glob=1 forces the global-memory (L2) weights path; m=64 needs it anyway
-    if glob:
+    # glob=1 forces the global-memory (L2) weights path; m=64 needs it anyway;
+    # "wide" forces 16-warp blocks (the 512-thread RL instantiation)
+    if glob == "wide":
+        monkeypatch.setenv("RS_WARPS_PER_BLOCK", "16")
+    elif glob:
         monkeypatch.setenv("RS_RL_GLOBAL", "1")
     sd = abi.state_dimension(m)
     rng = np.random.default_rng(m)
