@@ -573,60 +573,53 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
         if (!act[g]) continue;
         Inst& I = S[g];
         const int i = g * W + l;
-        // The lane keeps stepping its instance until its clock reaches t1 or
-        // a step raises an event (the warp handles events before that
-        // instance steps again); instances are independent within a tick.
-        for (;;) {
-          if (I.n == 0 && I.w_cnt == 0) {  // emptied by last iteration's events
-            I.clock = t1;
-            act[g] = false;
-            break;
+        if (I.n == 0 && I.w_cnt == 0) {  // emptied by last iteration's events
+          I.clock = t1;
+          act[g] = false;
+          continue;
+        }
+        if (I.w_cnt > 0 && I.n < P.max_batch) {
+          const int w0 = I.w_cnt + I.o_cnt;
+          lane_admit(P, gw, off, i, I);
+          wdelta += I.w_cnt + I.o_cnt - w0;
+        }
+        if (I.n == 0) {  // logic_error, instance.hpp:209-211
+          ev = true;
+          evg |= 1u << g;
+          continue;
+        }
+        if (I.npf > 0) {  // whole-prompt prefill; co-running decodes stall
+          I.clock = __dadd_rn(I.clock, __dadd_rn(__dadd_rn(P.intercept,
+                                                           __dmul_rn(P.tpp, (double)I.pend)),
+                                                 __dmul_rn(P.dpt, (double)I.kv)));
+          I.kv += I.pend;
+          I.pend = 0;
+          I.npf = 0;
+          if (I.kv > P.kv_cap && I.n > 1) { ev = true; evg |= 1u << g; }
+        } else {  // every running request emits one token
+          const int n = I.n;
+          if (n != I.el_n) {
+            I.dec_el = __dadd_rn(P.dtb, __dmul_rn(P.dpt, (double)n));
+            I.el_n = n;
           }
-          if (I.w_cnt > 0 && I.n < P.max_batch) {
-            const int w0 = I.w_cnt + I.o_cnt;
-            lane_admit(P, gw, off, i, I);
-            wdelta += I.w_cnt + I.o_cnt - w0;
+          I.clock = __dadd_rn(I.clock, I.dec_el);
+          I.D++;
+          I.kv += n;
+          I.tleft -= n;
+          I.tok += n;
+          I.res += I.nge;
+          I.dleft -= n - I.nge;
+          if (I.ft < n) {  // first tokens of requests admitted since the last decode
+            for (int j = I.ft; j < n; ++j) {
+              const int q = RQ(P, gw, i, j);
+              if (q & kFresh) P.o_first[off + (q & kReqMask)] = I.clock;
+            }
+            I.ft = n;
           }
-          if (I.n == 0) {  // logic_error, instance.hpp:209-211
+          if (I.D >= I.next_done || I.D >= I.next_ge || (I.kv > P.kv_cap && n > 1)) {
             ev = true;
             evg |= 1u << g;
-            break;
           }
-          if (I.npf > 0) {  // whole-prompt prefill; co-running decodes stall
-            I.clock = __dadd_rn(I.clock, __dadd_rn(__dadd_rn(P.intercept,
-                                                             __dmul_rn(P.tpp, (double)I.pend)),
-                                                   __dmul_rn(P.dpt, (double)I.kv)));
-            I.kv += I.pend;
-            I.pend = 0;
-            I.npf = 0;
-            if (I.kv > P.kv_cap && I.n > 1) { ev = true; evg |= 1u << g; break; }
-          } else {  // every running request emits one token
-            const int n = I.n;
-            if (n != I.el_n) {
-              I.dec_el = __dadd_rn(P.dtb, __dmul_rn(P.dpt, (double)n));
-              I.el_n = n;
-            }
-            I.clock = __dadd_rn(I.clock, I.dec_el);
-            I.D++;
-            I.kv += n;
-            I.tleft -= n;
-            I.tok += n;
-            I.res += I.nge;
-            I.dleft -= n - I.nge;
-            if (I.ft < n) {  // first tokens of requests admitted since the last decode
-              for (int j = I.ft; j < n; ++j) {
-                const int q = RQ(P, gw, i, j);
-                if (q & kFresh) P.o_first[off + (q & kReqMask)] = I.clock;
-              }
-              I.ft = n;
-            }
-            if (I.D >= I.next_done || I.D >= I.next_ge || (I.kv > P.kv_cap && n > 1)) {
-              ev = true;
-              evg |= 1u << g;
-              break;
-            }
-          }
-          if (!(I.clock < t1)) break;
         }
       }
       // a stepped instance steps again while its clock is behind t1 (it has
