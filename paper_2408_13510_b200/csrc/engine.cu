@@ -718,7 +718,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     const int max_wpb = wide ? 16 : 8;
     KernelFn narrow = pl.kern;
     for (int wpb = max_wpb; wpb >= 1; --wpb) {
-      if (wpb_env && wpb != std::min(wpb_env, max_wpb)) continue;
+      if (wpb_env && wpb > wpb_env) continue;  // RS_WARPS_PER_BLOCK: an upper bound
       // wide RL blocks only in whole multiples of the 4 SM sub-partitions:
       // 9 warps would put 3 replays on one scheduler and 2 on the others,
       // and the slowest scheduler's replays set the tail (measured on c3)

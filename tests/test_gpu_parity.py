@@ -121,6 +121,7 @@ def test_rl_router_matches_oracle(gpu, m, eps, glob, monkeypatch):
     # "wide" forces 16-warp blocks (the 512-thread RL instantiation)
     if glob == "wide":
         monkeypatch.setenv("RS_WARPS_PER_BLOCK", "16")
+        monkeypatch.setenv("RS_WAIT_RING", "8")  # small replay slots: 16 fit next to the net
     elif glob:
         monkeypatch.setenv("RS_RL_GLOBAL", "1")
     sd = abi.state_dimension(m)
