@@ -131,6 +131,7 @@ struct KParams {
   const int* resident;
   // ClusterConfig::record_trajectory (general kernel only): per-tick reward
   // (env.hpp:257-303) and TickRecords (env.hpp:305-319)
+  const int2* vinfo;    // fast kernel: per-replay {bad, vmax} from validate_kernel (null: walk the trace)
   rs_trajectory traj;   // device arrays (by value); traj_on = 0: off
   int traj_on;
   double r_w, c_k;      // RewardConfig::r_w, shaping_coefficient(episode_k)

@@ -213,7 +213,7 @@ int64_t heavy_cutoff(const rs_profile& p, const rs_thresholds& t) {
 }
 
 struct WsLayout {
-  size_t counter, next, prev, emit, removed, wt, total;
+  size_t counter, next, prev, emit, removed, wt, vinfo, total;
 };
 
 size_t rl_param_count(const rs_batch_cfg& c) {
@@ -224,7 +224,7 @@ size_t rl_param_count(const rs_batch_cfg& c) {
   return w;
 }
 
-WsLayout ws_layout(int64_t total_requests, size_t rl_params = 0) {
+WsLayout ws_layout(int64_t total_requests, int64_t num_replays, size_t rl_params = 0) {
   WsLayout w;
   size_t off = 0;
   w.wt = off;  // transposed Q-network (global-weights mode), may be empty
@@ -239,6 +239,8 @@ WsLayout ws_layout(int64_t total_requests, size_t rl_params = 0) {
   off = align_up(off + 4ull * total_requests, 256);
   w.removed = off;
   off = align_up(off + (size_t)total_requests, 256);
+  w.vinfo = off;
+  off = align_up(off + 8ull * (size_t)num_replays, 256);
   w.total = off;
   return w;
 }
@@ -379,7 +381,7 @@ rs_status rs_workspace_size(const rs_batch_cfg* cfg, int32_t num_replays,
   if (s != RS_OK) return s;
   if (!bytes || num_replays < 0 || total_requests < 0)
     return fail(RS_ERR_INVALID_ARGUMENT, "bad workspace query");
-  *bytes = ws_layout(total_requests, rl_param_count(*cfg)).total;
+  *bytes = ws_layout(total_requests, num_replays, rl_param_count(*cfg)).total;
   return RS_OK;
 }
 
@@ -489,7 +491,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     return fail(RS_ERR_INVALID_ARGUMENT, "rs_replay_batch needs every per-request output array");
   if (cfg->policy == RS_POLICY_RL && cfg->rl_epsilon > 0.0 && !tr->policy_seed)
     return fail(RS_ERR_INVALID_ARGUMENT, "epsilon-greedy needs trace->policy_seed");
-  const WsLayout wl = ws_layout(tr->total_requests, rl_param_count(*cfg));
+  const WsLayout wl = ws_layout(tr->total_requests, tr->num_replays, rl_param_count(*cfg));
   if (!workspace || workspace_bytes < wl.total)
     return fail(RS_ERR_INVALID_ARGUMENT, "workspace too small (rs_workspace_size)");
   cudaStream_t st = (cudaStream_t)stream;
@@ -795,6 +797,24 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
             cfg->policy, (int)fast, groups, pl.width, pl.wpb, pl.per_sm, pl.block_smem,
             L.group_bytes, L.weights_bytes, pl.capacity);
   RS_CUDA(cudaMemsetAsync(kp.work_counter, 0, sizeof(int), st));
+  if (fast && !resident && env_int("RS_NO_VALIDATE_PASS", 0) == 0) {
+    // resident inputs: validation + preemption-counter zeroing as one
+    // parallel pass instead of a serial walk per replay warp
+    rs::ValidateParams vp;
+    vp.num_replays = tr->num_replays;
+    vp.offsets = kp.offsets;
+    vp.arrival = kp.arrival;
+    vp.prompt = kp.prompt;
+    vp.decode = kp.decode;
+    vp.ub_max = kp.ub_max;
+    vp.o_preempt = kp.o_preempt;
+    vp.mm_removed = cfg->policy == RS_POLICY_MIN_MIN ? kp.mm_removed : nullptr;
+    vp.vinfo = reinterpret_cast<int2*>(ws + wl.vinfo);
+    const int vgrid = std::max(1, std::min(tr->num_replays, sms * 8));
+    rs::validate_kernel<<<vgrid, rs::kStatsThreads, 0, st>>>(vp);
+    RS_CUDA(cudaGetLastError());
+    kp.vinfo = vp.vinfo;
+  }
   rs_status s2 = launch_kernel(pl.kern, kp, pl.wpb, rs::kWarp / pl.width, pl.block_smem,
                                tr->num_replays, st);
   if (s2 != RS_OK) return s2;

@@ -406,7 +406,11 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
 
   bool bad = false;
   int vmax = 0;
-  for (int j = l; j < R.n; j += W) {
+  if (!init && P.vinfo) {  // validated and zeroed by the validate_kernel pre-pass
+    const int2 v = P.vinfo[r];
+    bad = v.x != 0;
+    vmax = v.y;
+  } else for (int j = l; j < R.n; j += W) {
     const long long g = off + j;
     if (init) {
       P.o_instance[g] = -1;
