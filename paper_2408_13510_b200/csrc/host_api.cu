@@ -49,6 +49,8 @@ struct DeviceCache {
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
   int* marks = nullptr;                    // pinned residency watermarks
   int nmarks = 0;
+  cudaGraphExec_t gexec = nullptr;         // captured rs_replay_batch_host call
+  std::vector<char> gkey, warm_key;        // its shape / pointers; the last uncaptured call
 };
 DeviceCache g_cache[16];
 
@@ -223,130 +225,208 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
   const int64_t min_stream = se ? atoll(se) : (int64_t)1 << 22;
   const bool stream_in = uniform && n_eq > 0 && min_stream > 0 && N >= min_stream &&
                          rs_internal_fast_path(cfg) && !htraj;
-  RS_CUDA2(h2d(o_off, tr->offsets, 8ull * (R + 1)));
-  if (!stream_in) {
-    RS_CUDA2(h2d(o_arr, tr->arrival_s, 8ull * N));
-    RS_CUDA2(h2d(o_pr, tr->prompt_tokens, 4ull * N));
-    RS_CUDA2(h2d(o_de, tr->decode_tokens, 4ull * N));
-    RS_CUDA2(h2d(o_tk, tr->task, 1ull * N));
-  }
-  if (tr->given_bucket) RS_CUDA2(h2d(o_gv, tr->given_bucket, 1ull * N));
-  if (tr->predictor_seed) RS_CUDA2(h2d(o_ps, tr->predictor_seed, 8ull * R));
-  if (tr->policy_seed) RS_CUDA2(h2d(o_qs, tr->policy_seed, 8ull * R));
-  if (rl) RS_CUDA2(h2d(o_rl, cfg->rl_params, rl_bytes));
-
-  rs_batch_cfg dcfg = *cfg;
-  if (rl) dcfg.rl_params = reinterpret_cast<const double*>(b + o_rl);
-  rs_trace_soa dt = *tr;
-  dt.offsets = reinterpret_cast<const int64_t*>(b + o_off);
-  dt.arrival_s = reinterpret_cast<const double*>(b + o_arr);
-  dt.prompt_tokens = reinterpret_cast<const int32_t*>(b + o_pr);
-  dt.decode_tokens = reinterpret_cast<const int32_t*>(b + o_de);
-  dt.task = reinterpret_cast<const uint8_t*>(b + o_tk);
-  dt.given_bucket = tr->given_bucket ? reinterpret_cast<const uint8_t*>(b + o_gv) : nullptr;
-  dt.predictor_seed = tr->predictor_seed ? reinterpret_cast<const uint64_t*>(b + o_ps) : nullptr;
-  dt.policy_seed = tr->policy_seed ? reinterpret_cast<const uint64_t*>(b + o_qs) : nullptr;
-  rs_req_out dout;
-  dout.instance = reinterpret_cast<int32_t*>(b + o_in);
-  dout.routed_s = reinterpret_cast<double*>(b + o_ro);
-  dout.first_token_s = reinterpret_cast<double*>(b + o_fi);
-  dout.completion_s = reinterpret_cast<double*>(b + o_co);
-  dout.preemptions = reinterpret_cast<int32_t*>(b + o_pe);
-  dout.predicted_bucket = reinterpret_cast<uint8_t*>(b + o_pb);
-  rs_replay_stats* dstats = reinterpret_cast<rs_replay_stats*>(b + o_st);
-
-  dcfg.flags |= RS_FLAG_PREDICT_INLINE;  // predictions drawn inside the replay
-  rs_trajectory dtraj;
-  if (htraj) {
-    dtraj = *htraj;
-    void** dp[12] = {(void**)&dtraj.time_s, (void**)&dtraj.action, (void**)&dtraj.queue_penalty,
-                     (void**)&dtraj.completions, (void**)&dtraj.h, (void**)&dtraj.shaping_term,
-                     (void**)&dtraj.reward, (void**)&dtraj.infeasible_route,
-                     (void**)&dtraj.router_queue, (void**)&dtraj.tokens_emitted,
-                     (void**)&dtraj.instance_running, (void**)&dtraj.instance_waiting};
-    for (int k = 0; k < 12; ++k) *dp[k] = tf[k].host ? (void*)(b + tf[k].off) : nullptr;
-    if ((s = forward(rs_replay_trajectory(&dcfg, &dt, &dout, dstats, &dtraj, b + o_ws, ws_bytes,
-                                          st))) != RS_OK)
-      return s;
-  } else if (!stream_in) {
-    if ((s = forward(rs_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st))) !=
-        RS_OK)
-      return s;
-  } else {
-    // chunk boundaries: a small first chunk (the kernel starts on it), then
-    // x8 (each chunk lands well before the replays consume the previous one;
-    // few chunks = few 2D copy commands to queue)
-    std::vector<int> bounds;
-    for (int64_t e = std::min<int64_t>(n_eq, 256); ; e = std::min<int64_t>(n_eq, 8 * e)) {
-      bounds.push_back((int)e);
-      if (e == n_eq) break;
+  // Everything the call puts on the device, as one enqueue.  With pinned
+  // host buffers and a repeated call shape it is captured once into a CUDA
+  // graph and replayed with a single launch: the host does ~10 us of API
+  // work per call instead of ~3 ms of copy / launch calls, so a host-side
+  // stall (the host thread descheduled mid-enqueue, measured at up to 0.2 s
+  // on a shared box) no longer delays the device work.
+  auto w1 = w0;
+  auto enqueue = [&]() -> rs_status {
+    RS_CUDA2(h2d(o_off, tr->offsets, 8ull * (R + 1)));
+    if (!stream_in) {
+      RS_CUDA2(h2d(o_arr, tr->arrival_s, 8ull * N));
+      RS_CUDA2(h2d(o_pr, tr->prompt_tokens, 4ull * N));
+      RS_CUDA2(h2d(o_de, tr->decode_tokens, 4ull * N));
+      RS_CUDA2(h2d(o_tk, tr->task, 1ull * N));
     }
-    if (!dc.copy_stream)
-      RS_CUDA2(cudaStreamCreateWithFlags(&dc.copy_stream, cudaStreamNonBlocking));
-    if (!dc.ev_ready) RS_CUDA2(cudaEventCreateWithFlags(&dc.ev_ready, cudaEventDisableTiming));
-    if (!dc.ev_done) RS_CUDA2(cudaEventCreateWithFlags(&dc.ev_done, cudaEventDisableTiming));
-    if (dc.nmarks < (int)bounds.size()) {
-      if (dc.marks) cudaFreeHost(dc.marks);
-      dc.marks = nullptr;
-      dc.nmarks = 0;
-      RS_CUDA2(cudaMallocHost(&dc.marks, sizeof(int) * bounds.size()));
-      dc.nmarks = (int)bounds.size();
-    }
-    for (size_t i = 0; i < bounds.size(); ++i) dc.marks[i] = bounds[i];
-    int* flag = reinterpret_cast<int*>(b + o_fl);
-    RS_CUDA2(cudaMemsetAsync(flag, 0, sizeof(int), st));
-    RS_CUDA2(cudaEventRecord(dc.ev_ready, st));
-    const cudaStream_t cs = dc.copy_stream;
-    RS_CUDA2(cudaStreamWaitEvent(cs, dc.ev_ready, 0));
-    // The replay kernel is launched FIRST: it starts at once and gates each
-    // 32-request window on the watermark, so the host-side cost of queueing
-    // the chunk copies (and any host hiccup meanwhile) overlaps the replay
-    // instead of delaying its launch.  The stats pass waits for the copies.
-    s = forward(rs_internal_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st, flag,
-                                         kDeferStats, nullptr));
-    if (s != RS_OK) return s;
-    struct Col { size_t off; const void* src; size_t es; };
-    const Col cols[4] = {{o_arr, tr->arrival_s, 8}, {o_pr, tr->prompt_tokens, 4},
-                         {o_de, tr->decode_tokens, 4}, {o_tk, tr->task, 1}};
-    int lo = 0;
-    for (size_t i = 0; i < bounds.size(); ++i) {
-      const int hi = bounds[i];
-      for (const Col& c : cols) {
-        if (!c.src) continue;
-        const size_t pitch = (size_t)n_eq * c.es;
-        RS_CUDA2(cudaMemcpy2DAsync(b + c.off + (size_t)lo * c.es, pitch,
-                                   static_cast<const char*>(c.src) + (size_t)lo * c.es, pitch,
-                                   (size_t)(hi - lo) * c.es, (size_t)R, cudaMemcpyHostToDevice,
-                                   cs));
+    if (tr->given_bucket) RS_CUDA2(h2d(o_gv, tr->given_bucket, 1ull * N));
+    if (tr->predictor_seed) RS_CUDA2(h2d(o_ps, tr->predictor_seed, 8ull * R));
+    if (tr->policy_seed) RS_CUDA2(h2d(o_qs, tr->policy_seed, 8ull * R));
+    if (rl) RS_CUDA2(h2d(o_rl, cfg->rl_params, rl_bytes));
+
+    rs_batch_cfg dcfg = *cfg;
+    if (rl) dcfg.rl_params = reinterpret_cast<const double*>(b + o_rl);
+    rs_trace_soa dt = *tr;
+    dt.offsets = reinterpret_cast<const int64_t*>(b + o_off);
+    dt.arrival_s = reinterpret_cast<const double*>(b + o_arr);
+    dt.prompt_tokens = reinterpret_cast<const int32_t*>(b + o_pr);
+    dt.decode_tokens = reinterpret_cast<const int32_t*>(b + o_de);
+    dt.task = reinterpret_cast<const uint8_t*>(b + o_tk);
+    dt.given_bucket = tr->given_bucket ? reinterpret_cast<const uint8_t*>(b + o_gv) : nullptr;
+    dt.predictor_seed = tr->predictor_seed ? reinterpret_cast<const uint64_t*>(b + o_ps) : nullptr;
+    dt.policy_seed = tr->policy_seed ? reinterpret_cast<const uint64_t*>(b + o_qs) : nullptr;
+    rs_req_out dout;
+    dout.instance = reinterpret_cast<int32_t*>(b + o_in);
+    dout.routed_s = reinterpret_cast<double*>(b + o_ro);
+    dout.first_token_s = reinterpret_cast<double*>(b + o_fi);
+    dout.completion_s = reinterpret_cast<double*>(b + o_co);
+    dout.preemptions = reinterpret_cast<int32_t*>(b + o_pe);
+    dout.predicted_bucket = reinterpret_cast<uint8_t*>(b + o_pb);
+    rs_replay_stats* dstats = reinterpret_cast<rs_replay_stats*>(b + o_st);
+
+    dcfg.flags |= RS_FLAG_PREDICT_INLINE;  // predictions drawn inside the replay
+    rs_trajectory dtraj;
+    if (htraj) {
+      dtraj = *htraj;
+      void** dp[12] = {(void**)&dtraj.time_s, (void**)&dtraj.action, (void**)&dtraj.queue_penalty,
+                       (void**)&dtraj.completions, (void**)&dtraj.h, (void**)&dtraj.shaping_term,
+                       (void**)&dtraj.reward, (void**)&dtraj.infeasible_route,
+                       (void**)&dtraj.router_queue, (void**)&dtraj.tokens_emitted,
+                       (void**)&dtraj.instance_running, (void**)&dtraj.instance_waiting};
+      for (int k = 0; k < 12; ++k) *dp[k] = tf[k].host ? (void*)(b + tf[k].off) : nullptr;
+      if ((s = forward(rs_replay_trajectory(&dcfg, &dt, &dout, dstats, &dtraj, b + o_ws, ws_bytes,
+                                            st))) != RS_OK)
+        return s;
+    } else if (!stream_in) {
+      if ((s = forward(rs_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st))) !=
+          RS_OK)
+        return s;
+    } else {
+      // chunk boundaries: a small first chunk (the kernel starts on it), then
+      // x8 (each chunk lands well before the replays consume the previous one;
+      // few chunks = few 2D copy commands to queue)
+      std::vector<int> bounds;
+      for (int64_t e = std::min<int64_t>(n_eq, 256); ; e = std::min<int64_t>(n_eq, 8 * e)) {
+        bounds.push_back((int)e);
+        if (e == n_eq) break;
       }
-      RS_CUDA2(cudaMemcpyAsync(flag, dc.marks + i, sizeof(int), cudaMemcpyHostToDevice, cs));
-      lo = hi;
+      if (!dc.copy_stream)
+        RS_CUDA2(cudaStreamCreateWithFlags(&dc.copy_stream, cudaStreamNonBlocking));
+      if (!dc.ev_ready) RS_CUDA2(cudaEventCreateWithFlags(&dc.ev_ready, cudaEventDisableTiming));
+      if (!dc.ev_done) RS_CUDA2(cudaEventCreateWithFlags(&dc.ev_done, cudaEventDisableTiming));
+      if (dc.nmarks < (int)bounds.size()) {
+        if (dc.marks) cudaFreeHost(dc.marks);
+        dc.marks = nullptr;
+        dc.nmarks = 0;
+        RS_CUDA2(cudaMallocHost(&dc.marks, sizeof(int) * bounds.size()));
+        dc.nmarks = (int)bounds.size();
+      }
+      for (size_t i = 0; i < bounds.size(); ++i) dc.marks[i] = bounds[i];
+      int* flag = reinterpret_cast<int*>(b + o_fl);
+      RS_CUDA2(cudaMemsetAsync(flag, 0, sizeof(int), st));
+      RS_CUDA2(cudaEventRecord(dc.ev_ready, st));
+      const cudaStream_t cs = dc.copy_stream;
+      RS_CUDA2(cudaStreamWaitEvent(cs, dc.ev_ready, 0));
+      // The replay kernel is launched FIRST: it starts at once and gates each
+      // 32-request window on the watermark, so the host-side cost of queueing
+      // the chunk copies (and any host hiccup meanwhile) overlaps the replay
+      // instead of delaying its launch.  The stats pass waits for the copies.
+      s = forward(rs_internal_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st, flag,
+                                           kDeferStats, nullptr));
+      if (s != RS_OK) return s;
+      struct Col { size_t off; const void* src; size_t es; };
+      const Col cols[4] = {{o_arr, tr->arrival_s, 8}, {o_pr, tr->prompt_tokens, 4},
+                           {o_de, tr->decode_tokens, 4}, {o_tk, tr->task, 1}};
+      int lo = 0;
+      for (size_t i = 0; i < bounds.size(); ++i) {
+        const int hi = bounds[i];
+        for (const Col& c : cols) {
+          if (!c.src) continue;
+          const size_t pitch = (size_t)n_eq * c.es;
+          RS_CUDA2(cudaMemcpy2DAsync(b + c.off + (size_t)lo * c.es, pitch,
+                                     static_cast<const char*>(c.src) + (size_t)lo * c.es, pitch,
+                                     (size_t)(hi - lo) * c.es, (size_t)R, cudaMemcpyHostToDevice,
+                                     cs));
+        }
+        RS_CUDA2(cudaMemcpyAsync(flag, dc.marks + i, sizeof(int), cudaMemcpyHostToDevice, cs));
+        lo = hi;
+      }
+      RS_CUDA2(cudaEventRecord(dc.ev_done, cs));
+      s = forward(rs_internal_stats(&dt, &dout, dstats, st, dc.ev_done));
+      if (s != RS_OK) {
+        cudaStreamSynchronize(cs);
+        return s;
+      }
     }
-    RS_CUDA2(cudaEventRecord(dc.ev_done, cs));
-    s = forward(rs_internal_stats(&dt, &dout, dstats, st, dc.ev_done));
-    if (s != RS_OK) {
-      cudaStreamSynchronize(cs);
-      return s;
+    if (dbg) cudaEventRecord(tev[1], st);
+    w1 = std::chrono::steady_clock::now();
+    auto d2h = [&](void* dst, size_t off, size_t n) -> cudaError_t {
+      if (!dst || n == 0) return cudaSuccess;
+      return cudaMemcpyAsync(dst, b + off, n, cudaMemcpyDeviceToHost, st);
+    };
+    if (out) {
+      RS_CUDA2(d2h(out->instance, o_in, 4ull * N));
+      RS_CUDA2(d2h(out->routed_s, o_ro, 8ull * N));
+      RS_CUDA2(d2h(out->first_token_s, o_fi, 8ull * N));
+      RS_CUDA2(d2h(out->completion_s, o_co, 8ull * N));
+      RS_CUDA2(d2h(out->preemptions, o_pe, 4ull * N));
+      RS_CUDA2(d2h(out->predicted_bucket, o_pb, 1ull * N));
     }
-  }
-  if (dbg) cudaEventRecord(tev[1], st);
-  const auto w1 = std::chrono::steady_clock::now();
-  auto d2h = [&](void* dst, size_t off, size_t n) -> cudaError_t {
-    if (!dst || n == 0) return cudaSuccess;
-    return cudaMemcpyAsync(dst, b + off, n, cudaMemcpyDeviceToHost, st);
+    RS_CUDA2(d2h(stats, o_st, sizeof(rs_replay_stats) * R));
+    for (int k = 0; htraj && k < 12; ++k)
+      if (tf[k].host)
+        RS_CUDA2(d2h(const_cast<void*>(tf[k].host), tf[k].off, tf[k].es * tf[k].mult * (size_t)nrec));
+    return RS_OK;
   };
-  if (out) {
-    RS_CUDA2(d2h(out->instance, o_in, 4ull * N));
-    RS_CUDA2(d2h(out->routed_s, o_ro, 8ull * N));
-    RS_CUDA2(d2h(out->first_token_s, o_fi, 8ull * N));
-    RS_CUDA2(d2h(out->completion_s, o_co, 8ull * N));
-    RS_CUDA2(d2h(out->preemptions, o_pe, 4ull * N));
-    RS_CUDA2(d2h(out->predicted_bucket, o_pb, 1ull * N));
+  bool graphed = false;
+  if (!dbg && !htraj && getenv("RS_NO_GRAPH") == nullptr) {
+    auto pinned = [](const void* q) {
+      if (!q) return true;
+      cudaPointerAttributes a;
+      if (cudaPointerGetAttributes(&a, q) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+      }
+      return a.type == cudaMemoryTypeHost;
+    };
+    bool ok = pinned(tr->offsets) && pinned(tr->arrival_s) && pinned(tr->prompt_tokens) &&
+              pinned(tr->decode_tokens) && pinned(tr->task) && pinned(tr->given_bucket) &&
+              pinned(tr->predictor_seed) && pinned(tr->policy_seed) && pinned(stats) &&
+              (!rl || pinned(cfg->rl_params));
+    if (out)
+      ok = ok && pinned(out->instance) && pinned(out->routed_s) && pinned(out->first_token_s) &&
+           pinned(out->completion_s) && pinned(out->preemptions) && pinned(out->predicted_bucket);
+    if (ok) {
+      std::vector<char> key;
+      auto put = [&](const void* q, size_t n) {
+        key.insert(key.end(), static_cast<const char*>(q), static_cast<const char*>(q) + n);
+      };
+      rs_req_out ko{};
+      if (out) ko = *out;
+      put(cfg, sizeof(*cfg));
+      put(tr, sizeof(*tr));
+      put(&ko, sizeof(ko));
+      put(&stats, sizeof(stats));
+      put(&b, sizeof(b));
+      put(&o, sizeof(o));
+      put(&n_eq, sizeof(n_eq));
+      put(&stream_in, sizeof(stream_in));
+      if (dc.gexec && key == dc.gkey) {
+        RS_CUDA2(cudaGraphLaunch(dc.gexec, st));
+        graphed = true;
+      } else if (key == dc.warm_key) {  // second identical call: capture
+        if (dc.gexec) {
+          cudaGraphExecDestroy(dc.gexec);
+          dc.gexec = nullptr;
+          dc.gkey.clear();
+        }
+        cudaGraph_t g = nullptr;
+        if (cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) == cudaSuccess) {
+          const rs_status cs_ = enqueue();
+          const cudaError_t ce = cudaStreamEndCapture(st, &g);
+          if (cs_ == RS_OK && ce == cudaSuccess && g &&
+              cudaGraphInstantiate(&dc.gexec, g, 0) == cudaSuccess) {
+            dc.gkey = key;
+            graphed = cudaGraphLaunch(dc.gexec, st) == cudaSuccess;
+          }
+          if (g) cudaGraphDestroy(g);
+          if (!graphed) {  // fall back to direct enqueue
+            cudaGetLastError();
+            if (dc.gexec) cudaGraphExecDestroy(dc.gexec);
+            dc.gexec = nullptr;
+            dc.gkey.clear();
+            dc.warm_key.clear();
+          }
+        } else {
+          cudaGetLastError();
+        }
+      } else {
+        dc.warm_key = key;
+      }
+    }
   }
-  RS_CUDA2(d2h(stats, o_st, sizeof(rs_replay_stats) * R));
-  for (int k = 0; htraj && k < 12; ++k)
-    if (tf[k].host)
-      RS_CUDA2(d2h(const_cast<void*>(tf[k].host), tf[k].off, tf[k].es * tf[k].mult * (size_t)nrec));
+  if (!graphed && (s = enqueue()) != RS_OK) return s;
   if (dbg) cudaEventRecord(tev[2], st);
   RS_CUDA2(cudaStreamSynchronize(st));
   if (dbg) {

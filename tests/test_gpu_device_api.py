@@ -105,3 +105,41 @@ def test_fused_and_separate_predictor_paths_agree(gpu, pol):
         got.predicted = np.where(np.arange(sl.stop - sl.start) < sb[r]["injected"],
                                  got.predicted, 255).astype(np.uint8)
         assert O.compare(got, want) == [], r
+
+
+@pytest.mark.parametrize("streamed", [0, 1])
+def test_host_entry_graph_replay_matches_oracle(gpu, monkeypatch, streamed):
+    """rs_replay_batch_host with PINNED host buffers: the first call runs
+    directly, the second identical call is captured into a CUDA graph, later
+    calls replay it.  Every call's per-request outputs equal the oracle's,
+    with and without streamed input copies; fresh inputs in the same pinned
+    buffers flow through the replayed graph."""
+    import torch
+    monkeypatch.setenv("RS_STREAM_INPUTS", "1" if streamed else "0")
+    lib = gpu
+    R, n = 6, 400
+    cfg = abi.default_config("workload_aware", 4)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    outs = [torch.empty(R * n, dtype=d, pin_memory=True) for d in
+            (torch.int32, torch.float64, torch.float64, torch.float64, torch.int32, torch.uint8)]
+    stats = torch.zeros(R * 256, dtype=torch.uint8, pin_memory=True)
+    tb = engine.build_workload(range(1, R + 1), n, 30.0)
+    h = [pin(tb.offsets), pin(tb.arrival), pin(tb.prompt), pin(tb.decode), pin(tb.task)]
+    ps = pin(np.array([abi.mix_seed(s, 0x9DED) for s in range(1, R + 1)], np.uint64).view(np.int64))
+    tr = abi.TraceSoA(R, 0, R * n, *[x.data_ptr() for x in h], None, ps.data_ptr(), None)
+    ro = abi.ReqOut(*[o.data_ptr() for o in outs])
+    for call in range(4):
+        if call == 3:  # new trace contents in the same buffers
+            tb = engine.build_workload(range(11, 11 + R), n, 30.0)
+            for dst, src in zip(h[1:], (tb.arrival, tb.prompt, tb.decode, tb.task)):
+                dst.copy_(torch.from_numpy(src))
+        abi.check(lib, lib.rs_replay_batch_host(C.byref(cfg), C.byref(tr), C.byref(ro),
+                                                stats.data_ptr(), 0))
+        st = np.frombuffer(stats.numpy().tobytes(), dtype=abi.STATS_DTYPE)
+        arrs = [o.numpy() for o in outs]
+        for r in range(R):
+            s = slice(r * n, (r + 1) * n)
+            trr = O.Trace(tb.arrival[s], tb.prompt[s], tb.decode[s], tb.task[s])
+            want = O.ora_run(cfg, trr, int(ps.numpy().view(np.uint64)[r]))
+            got = O.ReplayResult(*[a[s] for a in arrs], st[r:r + 1])
+            assert O.compare(got, want) == [], (call, r)
