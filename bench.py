@@ -314,8 +314,9 @@ def main():
     gathered = torch.empty(world * R * 256, dtype=torch.uint8, device=dev) if world > 1 else None
 
     def step(ev=None):
-        # per cell one rs_replay_batch = the replay kernel (predictions drawn
-        # at injection) + the per-replay percentile kernel, on torch's stream
+        # per cell one rs_replay_batch = the validation pre-pass, the replay
+        # kernel (predictions drawn at injection) and the per-replay stats
+        # kernel, on torch's stream
         for k, c in enumerate(cells):
             if ev is not None:
                 ev[k].record(stream)
@@ -458,11 +459,11 @@ def main():
                    "parallelism": f"replay shards x{world} (weak)",
                    "prewarm_s": PREWARM_S},
         "decisions_per_step": ticks_total, "unfinished_replays": unfinished,
-        "gpu_launches": 2 * len(cells) * args.steps * world,
+        "gpu_launches": 3 * len(cells) * args.steps * world,  # validate + replay + stats
         "kernel_ms": {"replay_batch": replay_s * 1e3},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": "rs::replay_fast_kernel (+ stats_kernel, timed together)",
+                     "kernel": "rs::replay_fast_kernel (+ validate_kernel and stats_kernel, timed together)",
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "peak_source": peak_src},
         "clocks": clk.summary(),
