@@ -275,30 +275,30 @@ using KernelFn = void (*)(rs::KParams);
 // parallel) instantiates that policy's general and fast replay kernels.
 namespace rs {
 using KernelFn = void (*)(KParams);
-KernelFn kernel_for_0(bool fast, int groups, int width, bool wide);
-KernelFn kernel_for_1(bool fast, int groups, int width, bool wide);
-KernelFn kernel_for_2(bool fast, int groups, int width, bool wide);
-KernelFn kernel_for_3(bool fast, int groups, int width, bool wide);
-KernelFn kernel_for_4(bool fast, int groups, int width, bool wide);
-KernelFn kernel_for_5(bool fast, int groups, int width, bool wide);
-KernelFn kernel_for_6(bool fast, int groups, int width, bool wide);
-KernelFn kernel_for_7(bool fast, int groups, int width, bool wide);
-KernelFn kernel_for_8(bool fast, int groups, int width, bool wide);
+KernelFn kernel_for_0(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_1(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_2(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_3(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_4(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_5(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_6(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_7(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_8(bool fast, int groups, int width, int variant);
 }  // namespace rs
 
 namespace {
 
-KernelFn kernel_for(int policy, bool fast, int groups, int width, bool wide = false) {
+KernelFn kernel_for(int policy, bool fast, int groups, int width, int variant = 0) {
   switch (policy) {
-    case 0: return rs::kernel_for_0(fast, groups, width, wide);
-    case 1: return rs::kernel_for_1(fast, groups, width, wide);
-    case 2: return rs::kernel_for_2(fast, groups, width, wide);
-    case 3: return rs::kernel_for_3(fast, groups, width, wide);
-    case 4: return rs::kernel_for_4(fast, groups, width, wide);
-    case 5: return rs::kernel_for_5(fast, groups, width, wide);
-    case 6: return rs::kernel_for_6(fast, groups, width, wide);
-    case 7: return rs::kernel_for_7(fast, groups, width, wide);
-    case 8: return rs::kernel_for_8(fast, groups, width, wide);
+    case 0: return rs::kernel_for_0(fast, groups, width, variant);
+    case 1: return rs::kernel_for_1(fast, groups, width, variant);
+    case 2: return rs::kernel_for_2(fast, groups, width, variant);
+    case 3: return rs::kernel_for_3(fast, groups, width, variant);
+    case 4: return rs::kernel_for_4(fast, groups, width, variant);
+    case 5: return rs::kernel_for_5(fast, groups, width, variant);
+    case 6: return rs::kernel_for_6(fast, groups, width, variant);
+    case 7: return rs::kernel_for_7(fast, groups, width, variant);
+    case 8: return rs::kernel_for_8(fast, groups, width, variant);
   }
   return nullptr;
 }
@@ -714,7 +714,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     pl.width = width;
     pl.kern = kernel_for(cfg->policy, fast, groups, width);
     if (!pl.kern) return pl;
-    KernelFn wide = kernel_for(cfg->policy, fast, groups, width, true);
+    KernelFn wide = kernel_for(cfg->policy, fast, groups, width, 1);
     const int gpw = rs::kWarp / width;
     // the wide RL instantiation takes blocks of up to 16 warps
     const int max_wpb = wide ? 16 : 8;
@@ -785,6 +785,19 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
           pl.wpb = wpb;
           pl.block_smem = L.weights_bytes + wpb * L.group_bytes;
           pl.kern = kernel_for(cfg->policy, fast, groups, pl.width);  // <= 8 warps
+          // one block per SM: the uncapped-register build, when it fits
+          KernelFn lat = env_int("RS_NO_LAT_KERNEL", 0) ? nullptr
+                                                         : kernel_for(cfg->policy, fast, groups,
+                                                                      pl.width, 2);
+          int lat_blocks = 0;
+          if (lat &&
+              cudaFuncSetAttribute(lat, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   pl.block_smem) == cudaSuccess &&
+              cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lat_blocks, lat, wpb * rs::kWarp,
+                                                            (size_t)pl.block_smem) == cudaSuccess &&
+              lat_blocks >= 1)
+            pl.kern = lat;
+          cudaGetLastError();
           break;
         }
       }

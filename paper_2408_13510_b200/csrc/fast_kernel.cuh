@@ -745,6 +745,15 @@ __global__ void __launch_bounds__(256) replay_fast_kernel(const __grid_constant_
   replay_fast_body<POL, G, W>(P);
 }
 
+// Latency regime (every replay resident in one wave, <= 8 warps per SM):
+// no launch bound, so ptxas keeps the whole tick loop in registers (158 for
+// workload_aware, no spills) instead of capping at 128 with ~450 B of spill
+// traffic on the tick chain; one such block per SM fits the register file.
+template <int POL, int G, int W>
+__global__ void replay_fast_kernel_lat(const __grid_constant__ KParams P) {
+  replay_fast_body<POL, G, W>(P);
+}
+
 // Up to 16 (the RL policy in the throughput regime): its Q-network is staged
 // once per block, so one wide block per SM leaves the most shared memory for
 // replay slots (512 threads x 128 registers = the register file).  A separate
