@@ -201,6 +201,41 @@ def cpu_reference(cfgname, sample_replays, threads):
     return ticks / wall, ticks, wall, what
 
 
+def cpu_port_scan_free(cfgname, sample_replays, threads):
+    """The plain-C restatement (oracle/rs_oracle.c: the same tick loop without
+    the reference's O(N) per-tick reward scan, env.hpp:289-298 — the work the
+    GPU engine does) on host threads over the same bounded sample as
+    cpu_reference: the like-for-like CPU figure."""
+    from concurrent.futures import ThreadPoolExecutor
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracles as O  # baseline infrastructure
+    from paper_2408_13510_b200 import abi, engine
+    n, R, m, rates, pols, weights, desc = cfg_shape(cfgname)
+    per = max(1, sample_replays)
+    ticks = 0
+    wall = 0.0
+    for pi, policy in enumerate(pols):
+        pick = [rates[(pi + k * max(1, len(rates) // per)) % len(rates)] for k in range(per)]
+        traces = []
+        for k, rate in enumerate(pick):
+            t = engine.build_workload([k + 1], n, rate, weights)
+            traces.append(O.Trace(t.arrival, t.prompt, t.decode, t.task))
+        cfg = abi.default_config(policy, m)
+        keep = None
+        if policy == "rl":
+            dims, params = agent_for(m)
+            keep = abi.set_rl(cfg, dims, params)
+        O.ora_lib()
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(threads) as ex:  # ctypes releases the GIL
+            res = list(ex.map(lambda k: O.ora_run(cfg, traces[k], abi.mix_seed(k + 1, 0x9DED)),
+                              range(per)))
+        wall += time.perf_counter() - t0
+        ticks += sum(int(r.stats["ticks"][0]) for r in res)
+        del keep
+    return ticks / wall, ticks, wall
+
+
 def run_reference_impl(args, cfgname):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -507,6 +542,14 @@ def main():
         except Exception as e:  # baseline is reported, never the target
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
+        try:
+            pv, pticks, pwall = cpu_port_scan_free(args.config, sample, threads)
+            line["cpu_baseline_scan_free"] = {
+                "value": pv, "unit": UNIT, "cores": min(threads, sample), "kind": "port",
+                "sample": f"same sample, oracle/rs_oracle.c (no per-tick reward scan), "
+                          f"{pwall:.1f} s wall, {pticks} decisions"}
+        except Exception as e:
+            line["cpu_baseline_scan_free"] = {"value": None, "sample": f"unavailable: {e}"}
     print(json.dumps(line), flush=True)
     del keep
     if world > 1:
