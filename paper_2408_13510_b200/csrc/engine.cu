@@ -803,6 +803,22 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
       }
     }
   }
+  // Shared memory already limits the plan to one block of <= 8 warps per SM
+  // (e.g. the RL kernel with its staged Q-network): the register file is
+  // not the constraint, so take the uncapped-register build there too.
+  if (pl.width == rs::kWarp && pl.per_sm == 1 && pl.wpb <= 8 && pl.kern ==
+      kernel_for(cfg->policy, fast, groups, pl.width) && !env_int("RS_NO_LAT_KERNEL", 0)) {
+    KernelFn lat = kernel_for(cfg->policy, fast, groups, pl.width, 2);
+    int lat_blocks = 0;
+    if (lat &&
+        cudaFuncSetAttribute(lat, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.block_smem) ==
+            cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lat_blocks, lat, pl.wpb * rs::kWarp,
+                                                      (size_t)pl.block_smem) == cudaSuccess &&
+        lat_blocks >= 1)
+      pl.kern = lat;
+    cudaGetLastError();
+  }
   if (env_int("RS_DEBUG_PLAN", 0))
     fprintf(stderr,
             "rs plan: policy %d fast %d groups %d width %d wpb %d blocks/SM %d block_smem %d "
