@@ -501,6 +501,14 @@ def main():
                      "kernel": "rs::replay_fast_kernel (+ validate_kernel and stats_kernel, timed together)",
                      "algorithmic_bytes_per_launch": alg_bytes,
                      "peak_source": peak_src},
+        # the binding constraint: a replay is a serial tick chain, so the step
+        # time is ~ (ticks of the longest replay) x (latency of one tick)
+        "tick_chain": {
+            "longest_replay_ticks": int(max(int(st["ticks"].max()) for st in cell_stats)),
+            "ns_per_tick_longest_replay": replay_s * 1e9 / max(
+                1, max(int(st["ticks"].max()) for st in cell_stats)),
+            "note": "kernel time / ticks of the longest replay; the HBM roofline "
+                    "fraction is small because the work is latency-bound, not bandwidth-bound"},
         "clocks": clk.summary(),
         "trace_gen_s": t_gen,
     }
