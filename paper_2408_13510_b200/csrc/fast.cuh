@@ -53,18 +53,7 @@ struct Inst {  // one instance, held in its lane's registers
   // the decode-step count D at which the next of them drops below e1 / e2
   // (decode_left falls by one per decode step).  Exact between events.
   int sb1, sb2, nx1, nx2;
-  // decode-step count at which the next event fires: min(next_done,
-  // next_ge, first D with kv > kv_cap while n > 1); valid while n, kv's slope
-  // and the event targets are unchanged (refreshed by set_ev after every
-  // admission / prefill / scan / preemption)
-  int ev_at;
 };
-
-__device__ __forceinline__ void set_ev(const KParams& P, Inst& I) {
-  int kv_at = kBig;
-  if (I.n > 1) kv_at = I.kv > P.kv_cap ? I.D : I.D + (P.kv_cap - I.kv) / I.n + 1;
-  I.ev_at = min(min(I.next_done, I.next_ge), kv_at);
-}
 
 // running entry fields (admission order) and waiting ring fields
 __device__ __forceinline__ int& RQ(const KParams& P, int gw, int i, int j) {
@@ -111,7 +100,6 @@ __device__ __forceinline__ void inst_init(Inst& I) {
   I.resw = I.pendw = I.dlw = I.tlw = I.tokw = 0;
   I.sb1 = I.sb2 = 0;
   I.nx1 = I.nx2 = kBig;
-  I.ev_at = kBig;
 }
 
 // state-bucket tracking of one running entry with decode_left dl at step D
@@ -455,7 +443,6 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
     I.next_ge = nxg;
     I.next_done = nxd;
     I.ft = I.n;  // every survivor has emitted
-    set_ev(P, I);
   }
 }
 
@@ -487,7 +474,6 @@ __device__ inline void lane_recount(const KParams& P, int gw, int i, Inst& I) {
   I.nge = nge;
   I.next_ge = nxg;
   I.next_done = nxd;
-  set_ev(P, I);
 }
 
 // preempt_if_needed (instance.hpp:282-299) by the owning lane.  Running is

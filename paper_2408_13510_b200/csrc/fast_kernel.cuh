@@ -599,7 +599,6 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
           I.kv += I.pend;
           I.pend = 0;
           I.npf = 0;
-          set_ev(P, I);  // admissions changed n / targets, the prefill kv
           if (I.kv > P.kv_cap && I.n > 1) { ev = true; evg |= 1u << g; }
         } else {  // every running request emits one token
           const int n = I.n;
@@ -621,7 +620,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
             }
             I.ft = n;
           }
-          if (I.D >= I.ev_at) {  // completion, estimate reached or KV overflow
+          if (I.D >= I.next_done || I.D >= I.next_ge || (I.kv > P.kv_cap && n > 1)) {
             ev = true;
             evg |= 1u << g;
           }
