@@ -367,6 +367,18 @@ rs_status rs_generate_mixture_batch(const rs_profile* profile,
                                     double* arrival_s, int32_t* prompt_tokens,
                                     int32_t* decode_tokens, uint8_t* task);
 
+/* EmpiricalPredictor::fit (predictor.hpp:119-142) on a training trace and
+ * predict() (predictor.hpp:146-158) resolved per (task, prompt band) into
+ * cfg->empirical_table, using cfg's predictor and band edges; sets
+ * cfg->predictor_mode = RS_PREDICTOR_EMPIRICAL. */
+rs_status rs_empirical_fit_trace(rs_batch_cfg* cfg, int64_t n, const int32_t* prompt_tokens,
+                                 const int32_t* decode_tokens, const uint8_t* task);
+
+/* run_experiment's empirical predictor (experiment.hpp:341-351): the fit on
+ * n_train (the reference uses 20000) Table-1-mixture requests drawn from
+ * Rng(mix_seed(seed, 0xF17)). */
+rs_status rs_empirical_fit(rs_batch_cfg* cfg, uint64_t seed, int64_t n_train);
+
 /* Mlp::random (mlp.hpp:32-45) as DqnAgent's constructor uses it
  * (dqn.hpp:60-65): Rng(seed), w = (2u - 1) * sqrt(2 / fan_in), b = 0. */
 rs_status rs_mlp_random_init(const int32_t* dims, int32_t num_layers, uint64_t seed,

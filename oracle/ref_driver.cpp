@@ -572,6 +572,34 @@ int ref_dqn_train(int32_t state_dim, int32_t actions, int32_t hidden, const doub
   }
 }
 
+// run_experiment's empirical predictor (experiment.hpp:341-351) with the
+// reference's own EmpiricalPredictor: fit on n_train Table-1 requests from
+// Rng(mix_seed(seed, 0xF17)), then predict() for every (task, band) at the
+// band's lowest prompt length.  table_out: [5][8] (bands < n_band_edges).
+int ref_empirical_table(const rs_batch_cfg* cfg, uint64_t seed, int64_t n_train,
+                        uint8_t* table_out) {
+  try {
+    HardwareProfile hp = to_profile(cfg->profile);
+    Thresholds th = to_thresholds(cfg->thresholds);
+    Rng rng(mix_seed(seed, 0xF17));
+    ArrivalSpec spec{ArrivalProcess::Poisson, 1.0};
+    auto training = generate_dataset_mixture(hp, th, static_cast<std::size_t>(n_train), spec, rng);
+    BucketScheme scheme;
+    scheme.edges.assign(cfg->predictor_edges, cfg->predictor_edges + cfg->n_predictor_edges);
+    std::vector<long long> bands(cfg->band_edges, cfg->band_edges + cfg->n_band_edges);
+    auto emp = EmpiricalPredictor::fit(training.requests, scheme, bands);
+    for (int t = 0; t < kTaskKindCount; ++t)
+      for (int b = 0; b < cfg->n_band_edges; ++b)
+        table_out[t * RS_MAX_BANDS + b] = static_cast<uint8_t>(
+            emp.predict(static_cast<TaskKind>(t),
+                        static_cast<int>(std::max<long long>(1, cfg->band_edges[b]))));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // CPU baseline: replays r in [0, R) of a CSR batch on `threads` host threads
 // (atomic work counter), outputs per replay stats only.  Returns wall seconds
 // (excluding nothing but thread start) or -1 on error.

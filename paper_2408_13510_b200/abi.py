@@ -344,6 +344,7 @@ EXPORTED_SYMBOLS = (
     "rs_heavy_decode_cutoff", "rs_host_alloc", "rs_host_free", "rs_mlp_random_init",
     "rs_replay_trajectory", "rs_replay_trajectory_host", "rs_emit_report",
     "rs_dqn_workspace_size", "rs_dqn_update", "rs_dqn_update_host",
+    "rs_empirical_fit", "rs_empirical_fit_trace",
 )
 
 
@@ -384,6 +385,9 @@ def _declare(lib: C.CDLL) -> None:
     lib.rs_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
     lib.rs_heavy_decode_cutoff.restype = C.c_int64
     lib.rs_heavy_decode_cutoff.argtypes = [P(Profile), P(Thresholds)]
+    lib.rs_empirical_fit.argtypes = [P(BatchCfg), C.c_uint64, C.c_int64]
+    lib.rs_empirical_fit_trace.argtypes = [P(BatchCfg), C.c_int64, C.c_void_p, C.c_void_p,
+                                           C.c_void_p]
     lib.rs_mlp_random_init.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p]
     lib.rs_host_alloc.restype = C.c_void_p
     lib.rs_host_alloc.argtypes = [C.c_size_t]

@@ -154,10 +154,10 @@ Mixture build(const rs_profile& p, const rs_thresholds& th, const double* w) {
   return mx;
 }
 
-// generate_mixture + assign_arrivals (workload.hpp:209-245)
-void generate(const Mixture& mx, uint64_t seed, int64_t n, double rate, int process,
-              double* arrival, int32_t* prompt, int32_t* decode, uint8_t* task) {
-  Source s(rs_mix_seed(seed, 0xB00C));  // build_workload, experiment.hpp:293
+// generate_mixture + assign_arrivals (workload.hpp:209-245) from Rng(rng_seed)
+void generate_raw(const Mixture& mx, uint64_t rng_seed, int64_t n, double rate, int process,
+                  double* arrival, int32_t* prompt, int32_t* decode, uint8_t* task) {
+  Source s(rng_seed);
   double total = 0.0;
   for (double w : mx.weights) total += w;
   const size_t kinds = mx.tasks.size();
@@ -181,9 +181,83 @@ void generate(const Mixture& mx, uint64_t seed, int64_t n, double rate, int proc
   }
 }
 
+// build_workload's stream: Rng(mix_seed(seed, 0xB00C)) (experiment.hpp:293)
+void generate(const Mixture& mx, uint64_t seed, int64_t n, double rate, int process,
+              double* arrival, int32_t* prompt, int32_t* decode, uint8_t* task) {
+  generate_raw(mx, rs_mix_seed(seed, 0xB00C), n, rate, process, arrival, prompt, decode, task);
+}
+
+// BucketScheme::bucket_of (predictor.hpp:34-40): last edge <= tokens
+int bucket_of_edges(const int64_t* edges, int n, int64_t tokens) {
+  int b = 0;
+  for (int i = 1; i < n; ++i)
+    if (tokens >= edges[i]) b = i;
+  return b;
+}
+
+// argmax with the lowest index on ties (std::max_element, predictor.hpp:168-170)
+int argmax_counts(const long long* v, int n) {
+  int best = 0;
+  for (int i = 1; i < n; ++i)
+    if (v[i] > v[best]) best = i;
+  return best;
+}
+
 }  // namespace
 
 extern "C" {
+
+// EmpiricalPredictor::fit (predictor.hpp:119-142) on a training trace, then
+// predict() (predictor.hpp:146-158: the (task, prompt band) cell's argmax,
+// else the task marginal's, else the global one) resolved for every cell into
+// cfg->empirical_table; sets predictor_mode = RS_PREDICTOR_EMPIRICAL.
+rs_status rs_empirical_fit_trace(rs_batch_cfg* cfg, int64_t n, const int32_t* prompt,
+                                 const int32_t* decode, const uint8_t* task) {
+  if (!cfg || n < 1 || !prompt || !decode || !task) return RS_ERR_INVALID_ARGUMENT;
+  const int nb = cfg->n_predictor_edges, nbands = cfg->n_band_edges;
+  if (nb < 1 || nb > RS_MAX_BUCKETS || nbands < 1 || nbands > RS_MAX_BANDS)
+    return RS_ERR_INVALID_ARGUMENT;
+  long long cells[RS_NUM_TASKS][RS_MAX_BANDS][RS_MAX_BUCKETS] = {};
+  bool seen[RS_NUM_TASKS][RS_MAX_BANDS] = {};
+  long long marg[RS_NUM_TASKS][RS_MAX_BUCKETS] = {};
+  bool tseen[RS_NUM_TASKS] = {};
+  long long global[RS_MAX_BUCKETS] = {};
+  for (int64_t i = 0; i < n; ++i) {
+    if (task[i] >= RS_NUM_TASKS) return RS_ERR_INVALID_ARGUMENT;
+    const int b = bucket_of_edges(cfg->predictor_edges, nb, decode[i]);
+    const int band = bucket_of_edges(cfg->band_edges, nbands, prompt[i]);
+    cells[task[i]][band][b] += 1;
+    seen[task[i]][band] = true;
+    marg[task[i]][b] += 1;
+    tseen[task[i]] = true;
+    global[b] += 1;
+  }
+  for (int t = 0; t < RS_NUM_TASKS; ++t)
+    for (int band = 0; band < RS_MAX_BANDS; ++band) {
+      int pred = 0;
+      if (band < nbands && seen[t][band]) pred = argmax_counts(cells[t][band], nb);
+      else if (tseen[t]) pred = argmax_counts(marg[t], nb);
+      else pred = argmax_counts(global, nb);
+      cfg->empirical_table[t][band] = static_cast<uint8_t>(pred);
+    }
+  cfg->predictor_mode = RS_PREDICTOR_EMPIRICAL;
+  return RS_OK;
+}
+
+// run_experiment's empirical predictor (experiment.hpp:341-351): fit on
+// n_train requests of the Table-1 mixture drawn from Rng(mix_seed(seed,
+// 0xF17)) (generate_dataset_mixture; arrival draws come after all token draws
+// and do not affect the fit).
+rs_status rs_empirical_fit(rs_batch_cfg* cfg, uint64_t seed, int64_t n_train) {
+  if (!cfg || n_train < 1) return RS_ERR_INVALID_ARGUMENT;
+  const Mixture mx = build(cfg->profile, cfg->thresholds, nullptr);
+  std::vector<double> arr(static_cast<size_t>(n_train));
+  std::vector<int32_t> pr(static_cast<size_t>(n_train)), de(static_cast<size_t>(n_train));
+  std::vector<uint8_t> tk(static_cast<size_t>(n_train));
+  generate_raw(mx, rs_mix_seed(seed, 0xF17), n_train, 1.0, 0, arr.data(), pr.data(), de.data(),
+               tk.data());
+  return rs_empirical_fit_trace(cfg, n_train, pr.data(), de.data(), tk.data());
+}
 
 rs_status rs_generate_mixture(const rs_profile* profile, const rs_thresholds* thresholds,
                               const double* task_weights, uint64_t seed, int64_t n,

@@ -335,3 +335,14 @@ def ref_dqn_train(dims, params, states, actions, rewards, next_states, dones, ba
     if rc != 0:
         raise RuntimeError(ref_error())
     return idx, losses, online, target
+
+
+def ref_empirical_table(cfg, seed, n_train=20000):
+    """The reference's EmpiricalPredictor fit + predict table ([5, 8] uint8)."""
+    lib = ref_lib()
+    lib.ref_empirical_table.argtypes = [C.POINTER(abi.BatchCfg), C.c_uint64, C.c_int64,
+                                        C.c_void_p]
+    out = np.zeros((abi.RS_NUM_TASKS, abi.RS_MAX_BANDS), np.uint8)
+    if lib.ref_empirical_table(C.byref(cfg), seed, n_train, out.ctypes.data) != 0:
+        raise RuntimeError(ref_error())
+    return out
