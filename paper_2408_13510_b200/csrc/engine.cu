@@ -562,6 +562,9 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     kp.ub[i] = (int)ub_of(*cfg, i);
   }
   kp.n_band_edges = cfg->n_band_edges;
+  for (int i = 0; i < cfg->n_band_edges && i < RS_MAX_BANDS; ++i)
+    kp.band_edges[i] = (int)cfg->band_edges[i];
+  std::memcpy(kp.emp_table, cfg->empirical_table, sizeof(kp.emp_table));  // fused predictor
   kp.predictor_mode = cfg->predictor_mode;
   kp.rcap = L.rcap;
   kp.wcap = L.wcap;
