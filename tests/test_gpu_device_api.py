@@ -143,3 +143,27 @@ def test_host_entry_graph_replay_matches_oracle(gpu, monkeypatch, streamed):
             want = O.ora_run(cfg, trr, int(ps.numpy().view(np.uint64)[r]))
             got = O.ReplayResult(*[a[s] for a in arrs], st[r:r + 1])
             assert O.compare(got, want) == [], (call, r)
+
+
+@pytest.mark.parametrize("mode", ["given", "empirical"])
+def test_fused_predictor_modes_match_separate_kernel(gpu, mode):
+    """The at-injection predictor in GIVEN and EMPIRICAL mode against the
+    standalone predict kernel (itself checked against the oracle above):
+    identical buckets and identical replays."""
+    import torch
+    seeds = list(range(40, 52))
+    tb = engine.build_workload(seeds, 900, 25.0)
+    ps = [abi.mix_seed(s, 0x9DED) for s in seeds]
+    cfg = abi.default_config("workload_aware", 4)
+    given = None
+    if mode == "given":
+        cfg.predictor_mode = abi.PRED_GIVEN
+        given = np.random.default_rng(3).integers(0, 4, tb.total).astype(np.uint8)
+    else:
+        abi.check(gpu, gpu.rs_empirical_fit(C.byref(cfg), 9, 20000))
+    bufs, tr = _dev_batch(torch, tb, ps, given)
+    a, sa = _replay(torch, gpu, cfg, tr, tb.total, tb.num_replays, True)
+    b, sb = _replay(torch, gpu, cfg, tr, tb.total, tb.num_replays, False)
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint8), y.view(np.uint8))
+    assert sa.tobytes() == sb.tobytes()
