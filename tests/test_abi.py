@@ -41,6 +41,9 @@ STRUCTS = {
     "rs_replay_stats": abi.ReplayStats,
     "rs_profile": abi.Profile,
     "rs_impact": abi.Impact,
+    "rs_trajectory": abi.Trajectory,
+    "rs_dqn_batch": abi.DqnBatch,
+    "rs_dqn_state": abi.DqnState,
 }
 
 
