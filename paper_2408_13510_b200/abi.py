@@ -14,7 +14,8 @@ from pathlib import Path
 import numpy as np
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "_lib" / "librs_b200.so"
+# RS_B200_LIB: load another build of the library (A/B timing of kernel variants)
+LIB_PATH = Path(os.environ.get("RS_B200_LIB", PKG_DIR / "_lib" / "librs_b200.so"))
 
 RS_ABI_VERSION = 1
 RS_MAX_BUCKETS = 8

@@ -53,6 +53,7 @@ struct Inst {  // one instance, held in its lane's registers
   // the decode-step count D at which the next of them drops below e1 / e2
   // (decode_left falls by one per decode step).  Exact between events.
   int sb1, sb2, nx1, nx2;
+  int ev_at;  // min(next_done, next_ge): the decode step of the next scan event
 };
 
 // running entry fields (admission order) and waiting ring fields
@@ -100,6 +101,7 @@ __device__ __forceinline__ void inst_init(Inst& I) {
   I.resw = I.pendw = I.dlw = I.tlw = I.tokw = 0;
   I.sb1 = I.sb2 = 0;
   I.nx1 = I.nx2 = kBig;
+  I.ev_at = kBig;
 }
 
 // state-bucket tracking of one running entry with decode_left dl at step D
@@ -230,6 +232,7 @@ __device__ __forceinline__ void lane_admit_one(const KParams& P, int gw, int i, 
   const int done_at = tru - emit + I.D;
   I.next_done = done_at < I.next_done ? done_at : I.next_done;
   sb_add(P, I, dhat - emit);
+  I.ev_at = min(I.next_done, I.next_ge);
   waitagg(I, prompt, dhat, tru, emit, -1);
 }
 
@@ -443,6 +446,7 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
     I.next_ge = nxg;
     I.next_done = nxd;
     I.ft = I.n;  // every survivor has emitted
+    I.ev_at = min(nxd, nxg);
   }
 }
 
@@ -474,6 +478,7 @@ __device__ inline void lane_recount(const KParams& P, int gw, int i, Inst& I) {
   I.nge = nge;
   I.next_ge = nxg;
   I.next_done = nxd;
+  I.ev_at = min(nxd, nxg);
 }
 
 // preempt_if_needed (instance.hpp:282-299) by the owning lane.  Running is

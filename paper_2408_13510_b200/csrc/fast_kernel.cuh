@@ -620,7 +620,9 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
             }
             I.ft = n;
           }
-          if (I.D >= I.next_done || I.D >= I.next_ge || (I.kv > P.kv_cap && n > 1)) {
+          // KV overflow needs n > 1, but a lone request never overflows: it
+          // was routed only if prompt + true decode fit (env.hpp:262-267)
+          if (I.D >= I.ev_at || I.kv > P.kv_cap) {
             ev = true;
             evg |= 1u << g;
           }
