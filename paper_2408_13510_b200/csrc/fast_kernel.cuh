@@ -582,17 +582,22 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
           act[g] = false;
           continue;
         }
+        // a prefill is only ever pending right after an admission, and an
+        // instance with an empty batch has waiting work (checked above), so
+        // the common decode step skips both tests
+        bool prefill = false;
         if (I.w_cnt > 0 && I.n < P.max_batch) {
           const int w0 = I.w_cnt + I.o_cnt;
           lane_admit(P, gw, off, i, I);
           wdelta += I.w_cnt + I.o_cnt - w0;
+          if (I.n == 0) {  // logic_error, instance.hpp:209-211
+            ev = true;
+            evg |= 1u << g;
+            continue;
+          }
+          prefill = I.npf > 0;
         }
-        if (I.n == 0) {  // logic_error, instance.hpp:209-211
-          ev = true;
-          evg |= 1u << g;
-          continue;
-        }
-        if (I.npf > 0) {  // whole-prompt prefill; co-running decodes stall
+        if (prefill) {  // whole-prompt prefill; co-running decodes stall
           I.clock = __dadd_rn(I.clock, __dadd_rn(__dadd_rn(P.intercept,
                                                            __dmul_rn(P.tpp, (double)I.pend)),
                                                  __dmul_rn(P.dpt, (double)I.kv)));
