@@ -630,6 +630,22 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
           if (I.D >= I.ev_at || I.kv > P.kv_cap) {
             ev = true;
             evg |= 1u << g;
+          } else if (I.w_cnt == 0 && I.clock < t1) {
+            // Nothing waits, so the next step of this instance is another
+            // pure decode step (no admission can precede it): take it now
+            // instead of in a further warp iteration (decode steps are
+            // ~17 ms against the 20 ms tick, so this is the common case).
+            I.clock = __dadd_rn(I.clock, I.dec_el);
+            I.D++;
+            I.kv += n;
+            I.tleft -= n;
+            I.tok += n;
+            I.res += I.nge;
+            I.dleft -= n - I.nge;
+            if (I.D >= I.ev_at || I.kv > P.kv_cap) {
+              ev = true;
+              evg |= 1u << g;
+            }
           }
         }
       }
