@@ -397,6 +397,7 @@ def main():
             dist.barrier()
     elapsed = start.elapsed_time(stop) / 1e3
     replay_s = sum(e[0].elapsed_time(e[-1]) for e in evs) / 1e3 / args.steps
+    step_ms = [round(e[0].elapsed_time(e[-1]), 3) for e in evs]
     cell_ms = [sum(e[k].elapsed_time(e[k + 1]) for e in evs) / args.steps
                for k in range(len(cells))]
     red_dev = dev if backend == "nccl" else "cpu"
@@ -495,7 +496,7 @@ def main():
                    "prewarm_s": PREWARM_S},
         "decisions_per_step": ticks_total, "unfinished_replays": unfinished,
         "gpu_launches": 3 * len(cells) * args.steps * world,  # validate + replay + stats
-        "kernel_ms": {"replay_batch": replay_s * 1e3},
+        "kernel_ms": {"replay_batch": replay_s * 1e3, "per_step": step_ms},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "rs::replay_fast_kernel (+ validate_kernel and stats_kernel, timed together)",
