@@ -86,9 +86,14 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """nvidia-smi clocks / throttle reasons during the timed region.
 
-    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+    Started before the warm-up (nvidia-smi's own start-up disturbs the GPU for
+    tens of ms: measured as a slow first timed step when it was started at
+    the timed region), stopped after it; only the samples whose timestamps
+    fall inside the timed window (`mark`) are summarised."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -96,17 +101,21 @@ class ClockSampler:
         self.gpus = gpus
         self.proc = None
         self.out = b""
+        self.window = None
 
-    def __enter__(self):
+    def start(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "200"], stdout=subprocess.PIPE,
-                                         stderr=subprocess.DEVNULL)
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
         return self
 
-    def __exit__(self, *a):
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def stop(self):
         if self.proc:
             self.proc.terminate()
             try:
@@ -115,22 +124,31 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
+        import datetime
         rows = []
         for line in self.out.decode(errors="replace").splitlines():
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 8 or not f[0].isdigit() or int(f[0]) not in self.gpus:
+            if len(f) < 9 or not f[1].isdigit() or int(f[1]) not in self.gpus:
                 continue
             try:
-                rows.append((int(f[1]), int(f[2]), f[4:8]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except ValueError:
+                ts = None
+            try:
+                rows.append((ts, int(f[2]), int(f[3]), f[5:9]))
             except ValueError:
                 continue
+        if self.window and rows:
+            t0, t1 = self.window
+            inside = [r for r in rows if r[0] is not None and t0 - 0.05 <= r[0] <= t1 + 0.25]
+            rows = inside or rows
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        load = [r for r in rows if r[0] > 500] or rows
+        load = [r for r in rows if r[1] > 500] or rows
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in load for i, v in enumerate(r[2]) if v == "Active"})
-        return {"sm_mhz": float(np.median([r[0] for r in load])),
-                "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons, "samples": len(load)}
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[3]) if v == "Active"})
+        return {"sm_mhz": float(np.median([r[1] for r in load])),
+                "sm_max_mhz": max(r[2] for r in rows), "reasons": reasons, "samples": len(load)}
 
 
 def make_workload(cfgname, rank, threads=0):
@@ -366,6 +384,8 @@ def main():
                 else:  # gloo gathers host tensors
                     gathered.copy_(rdist.gather_stats(c["st"].cpu(), world))
 
+    # clock sampler first: its start-up must not land in the timed region
+    clk = ClockSampler(list(range(world)) if world > 1 else [local]).start()
     # Pre-warm: a fresh box's first seconds of work run ~35% slower (clock /
     # power ramp; measured), so repeat untimed full steps for >= PREWARM_S
     # before the W warm-up steps.  Reported in config.prewarm_s.
@@ -387,14 +407,16 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(list(range(world)) if world > 1 else [local]) as clk:
-        start.record(stream)
-        for k in range(args.steps):
-            step(evs[k])
-        stop.record(stream)
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
+    t_win0 = time.time()
+    start.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    stop.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    clk.mark(t_win0, time.time())
+    clk.stop()
     elapsed = start.elapsed_time(stop) / 1e3
     replay_s = sum(e[0].elapsed_time(e[-1]) for e in evs) / 1e3 / args.steps
     step_ms = [round(e[0].elapsed_time(e[-1]), 3) for e in evs]
