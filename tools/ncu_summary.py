@@ -59,6 +59,20 @@ def main():
             s["dram_gbs"] = s["dram_bytes_per_launch"] / s["duration_ns"]
     if alg:
         s["algorithmic_bytes_per_launch"] = alg
+    # per-pipe issue utilisation (% of peak, active cycles): the FP64 pipe is
+    # the Q-network's roofline; ALU / branch / shared-memory show the tick chain
+    pipes = {}
+    for p in ("alu", "fma", "fp64", "lsu", "xu", "adu", "cbu", "uniform"):
+        v = num(f"sm__inst_executed_pipe_{p}.avg.pct_of_peak_sustained_active")
+        if v is not None:
+            pipes[p] = round(v, 2)
+    v = num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+    if v is not None:
+        pipes["fp64_cycles_active"] = round(v, 2)
+    v = num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")
+    if v is not None:
+        pipes["shared_wavefronts"] = round(v, 2)
+    s["pipe_utilisation_pct"] = pipes
     for k in hdr:
         if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
             v = num(k)
