@@ -53,8 +53,21 @@ __device__ __forceinline__ double mixing_for(const KParams& P, long long p, long
   return __dadd_rn(__dmul_rn(P.alpha, r_p), __dmul_rn(__dsub_rn(1.0, P.alpha), r_d));
 }
 
-__device__ __forceinline__ double round2(double x) {  // env.hpp:82
-  return __ddiv_rn(round(__dmul_rn(x, 100.0)), 100.0);
+// round2 (env.hpp:82): std::round(x * 100.0) / 100.0.  The quotient of the
+// integer k = round(x * 100) by 100 is formed without a division for
+// 0 < k <= 2^22 (every state feature: capacity in [0, 1], T^_c up to ~4e4 s):
+// q0 = k * RN(0.01), one exact FMA residual and one FMA correction give RN(k / 100)
+// (Markstein; checked for every k in the range, tools/check_round2.py).  Zero
+// keeps its sign (k / 100 = k); anything else divides.
+constexpr double kRound2FastMax = 4194304.0;  // 2^22
+__device__ __forceinline__ double round2(double x) {
+  const double k = round(__dmul_rn(x, 100.0));
+  if (k > 0.0 && k <= kRound2FastMax) {
+    const double q0 = __dmul_rn(k, 0.01);
+    const double r = __fma_rn(-q0, 100.0, k);
+    return __fma_rn(r, 0.01, q0);
+  }
+  return k == 0.0 ? k : __ddiv_rn(k, 100.0);
 }
 
 __device__ __forceinline__ InstHot load_inst(const Grp& G, int i) { return G.inst[i]; }
