@@ -171,8 +171,10 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
     }
     if (l == 0) {
       const int q = queue_len<POL>(R);
-      x[m * per] = __ddiv_rn((double)(q < 512 ? q : 512), 512.0);
-      x[m * per + 1] = has_head ? __ddiv_rn((double)hr.prompt, 1024.0) : 0.0;
+      // min(Q, 512) / 512 and prompt / 1024: power-of-two divisors of small
+      // integers, so the quotient is an exact multiply (no division sequence)
+      x[m * per] = __dmul_rn((double)(q < 512 ? q : 512), 0x1p-9);
+      x[m * per + 1] = has_head ? __dmul_rn((double)hr.prompt, 0x1p-10) : 0.0;
       x[m * per + 2] = has_head ? (double)hb : 0.0;
     }
     L.sync();

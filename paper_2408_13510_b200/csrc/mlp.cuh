@@ -102,9 +102,9 @@ constexpr int kMlpMaskWords = 4;
 constexpr int kMlpSmemMaxWidth = kMlpMaskWords * kWarp;
 
 // Forward with weights staged in shared memory (double index 0, W^T rows
-// [i][o]), x / h0 / h1 at double indices xd / h0d / h1d, and a per-warp list
-// of the current layer's nonzero inputs compacted in ascending index order as
-// 16-byte records {value, W^T row offset} at double index lvd + 2k (lvd even).
+// [i][o]), x at double index xd, and per warp two lists of a layer's nonzero
+// inputs in ascending index order as 16-byte records {value, W^T row offset}:
+// A at double index lvd + 2k, B over the h0 | h1 area from h0d (both even).
 // The accumulation is a counted loop over the nonzero terms only: each output
 // still adds w*x for i = 0..ni-1 in order, zero terms omitted exactly as in
 // mlp_forward_warp.  Layers with an even width and an even weight offset give
@@ -115,21 +115,19 @@ template <int W>
 __device__ inline int mlp_forward_list(const int* dims, const int* woff, const int* boff,
                                        int layers, int xd, int h0d, int h1d, int lvd,
                                        const Lanes<W>& L) {
+  (void)h1d;  // h0 | h1 (contiguous, 2 x maxw doubles) hold the second record list
   const int l = L.l;
   const unsigned lt = L.lt();
-  int cur = xd;
   unsigned long long best_key = 0;
   int best_idx = 0x7fffffff;
   bool have = false;
-  const double2* rec = reinterpret_cast<const double2*>(rs_smd + lvd);
-  for (int layer = 0; layer < layers; ++layer) {
-    const int ni = dims[layer], no = dims[layer + 1];
-    const int wt = woff[layer], bs = boff[layer];
-    // compact the nonzero inputs of `cur` into {value, row} records
-    int nnz = 0;
+  // the input layer's nonzero entries, compacted from x into list A
+  int nnz = 0;
+  {
+    const int ni = dims[0], no = dims[1], wt = woff[0];
     for (int c = 0; c < ni; c += W) {
       const int i = c + l;
-      const double v = i < ni ? rs_smd[cur + i] : 0.0;
+      const double v = i < ni ? rs_smd[xd + i] : 0.0;
       const bool nz = v != 0.0;
       const unsigned msk = L.ballot(nz);
       if (nz) {
@@ -140,15 +138,29 @@ __device__ inline int mlp_forward_list(const int* dims, const int* woff, const i
       nnz += __popc(msk);
     }
     L.sync();
+  }
+  for (int layer = 0; layer < layers; ++layer) {
+    const int no = dims[layer + 1];
+    const int wt = woff[layer], bs = boff[layer];
     const bool last = layer + 1 == layers;
-    const int dst = (layer & 1) ? h1d : h0d;
-    auto emit = [&](int o, double a) {
-      if (!last) {
-        rs_smd[dst + o] = a > 0.0 ? a : 0.0;
-      } else {  // running argmax, strict >: lower indices win ties
-        const unsigned long long k = ordered_key(a);
-        if (!have || k > best_key) { best_key = k; best_idx = o; have = true; }
-      }
+    // ping-pong: even layers read list A (lvd) and write B (h0d), odd ones
+    // the reverse.  A hidden layer's ReLU outputs go straight into the next
+    // layer's list: only the nonzero ones, in ascending output order, as
+    // {value, next layer's W^T row} records (the list the compaction of a
+    // stored h would build, without the store and re-read).
+    const int ind = (layer & 1) ? h0d : lvd;
+    const int outd = (layer & 1) ? lvd : h0d;
+    const double2* rec = reinterpret_cast<const double2*>(rs_smd + ind);
+    const int nwt = last ? 0 : woff[layer + 1];
+    const int nno = last ? 0 : dims[layer + 2];
+    int nout = 0;
+    auto put = [&](int p, int o, double a) {
+      rs_smd[outd + 2 * p] = a;
+      rs_smd[outd + 2 * p + 1] = __longlong_as_double((long long)(nwt + o * nno));
+    };
+    auto arg = [&](int o, double a) {  // running argmax, strict >: lower indices win ties
+      const unsigned long long k = ordered_key(a);
+      if (!have || k > best_key) { best_key = k; best_idx = o; have = true; }
     };
     if (((no | wt) & 1) == 0) {  // paired adjacent outputs
       for (int ob = 0; ob < no; ob += 2 * W) {
@@ -165,9 +177,16 @@ __device__ inline int mlp_forward_list(const int* dims, const int* woff, const i
           a0 = __dadd_rn(a0, __dmul_rn(w.x, r.x));
           a1 = __dadd_rn(a1, __dmul_rn(w.y, r.x));
         }
-        if (v) {
-          emit(o0, a0);
-          emit(o0 + 1, a1);
+        if (!last) {  // ReLU: a > 0 keeps a, anything else is an exact zero
+          const bool nz0 = v && a0 > 0.0, nz1 = v && a1 > 0.0;
+          const unsigned b0 = L.ballot(nz0), b1 = L.ballot(nz1);
+          const int p = nout + __popc(b0 & lt) + __popc(b1 & lt);
+          if (nz0) put(p, o0, a0);
+          if (nz1) put(p + (nz0 ? 1 : 0), o0 + 1, a1);
+          nout += __popc(b0) + __popc(b1);
+        } else if (v) {
+          arg(o0, a0);
+          arg(o0 + 1, a1);
         }
       }
     } else {  // one output per lane
@@ -182,11 +201,18 @@ __device__ inline int mlp_forward_list(const int* dims, const int* woff, const i
           const int row = (int)__double_as_longlong(r.y);
           a0 = __dadd_rn(a0, __dmul_rn(rs_smd[row + c0], r.x));
         }
-        if (v) emit(o0, a0);
+        if (!last) {
+          const bool nz0 = v && a0 > 0.0;
+          const unsigned b0 = L.ballot(nz0);
+          if (nz0) put(nout + __popc(b0 & lt), o0, a0);
+          nout += __popc(b0);
+        } else if (v) {
+          arg(o0, a0);
+        }
       }
     }
     L.sync();
-    cur = dst;
+    nnz = nout;
   }
   const unsigned long long gmax = L.max_u64(have ? best_key : 0ull);
   const int cand = (have && best_key == gmax) ? best_idx : 0x7fffffff;
