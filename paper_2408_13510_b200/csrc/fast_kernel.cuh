@@ -213,6 +213,11 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
     }
     unsigned long long bk = ~0ull;
     int bi = -1;
+    // G > 1: each lane first keeps the best of its own instances (lower g
+    // wins ties, i.e. the lower index), then ONE warp minimum; the lowest
+    // index holding it is the lowest g, then the lowest lane, among the lanes
+    // whose own best equals the minimum
+    int lg = -1;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int i = g * W + l;
@@ -244,10 +249,20 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
           k = ordered_key(__dsub_rn(__dadd_rn(avail, pcost), __dmul_rn(P.eps_s, mix)));
         }
       }
-      const int a = G == 1 ? argmin_narrow(L, k, v, P.mwidth) : grp_argmin_key(L, k, v);
-      if (a >= 0) {
-        const unsigned long long ka = L.shfl(k, a);
-        if (bi < 0 || ka < bk) { bk = ka; bi = g * W + a; }
+      if (G == 1) {
+        bi = argmin_narrow(L, k, v, P.mwidth);
+      } else if (v && (lg < 0 || k < bk)) {
+        bk = k;
+        lg = g;
+      }
+    }
+    if (G > 1) {
+      const bool lv = lg >= 0;
+      const unsigned long long mn = L.min_u64(lv ? bk : ~0ull);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const unsigned b = L.ballot(lv && lg == g && bk == mn);
+        if (bi < 0 && b) bi = g * W + __ffs(b) - 1;
       }
     }
     if (POL == RS_POLICY_JSQ || POL == RS_POLICY_MIN_MIN) return bi;
