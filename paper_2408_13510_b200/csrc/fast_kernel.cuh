@@ -36,6 +36,17 @@ __device__ __forceinline__ FeatI feat_of(const Inst& I) {
 template <int W>
 __device__ __forceinline__ int argmin_narrow(const Lanes<W>& L, unsigned long long key, bool valid,
                                              int width) {
+  if (W == kWarp) {
+    // whole warp: two 32-bit warp-minimum reductions (high word, then the low
+    // word among the lanes tied on it) instead of log2(width) 64-bit shuffles
+    const unsigned long long k = valid ? key : ~0ull;
+    const unsigned hi = (unsigned)(k >> 32);
+    const unsigned mh = __reduce_min_sync(kFull, hi);
+    const bool tie = hi == mh;
+    const unsigned ml = __reduce_min_sync(kFull, tie ? (unsigned)k : 0xffffffffu);
+    const unsigned ok = L.ballot(valid && tie && (unsigned)k == ml);
+    return ok ? __ffs(ok) - 1 : -1;
+  }
   unsigned long long k = valid ? key : ~0ull;
   for (int o = width >> 1; o > 0; o >>= 1) {
     const unsigned long long w = L.shfl_xor(k, o);
