@@ -231,21 +231,20 @@ struct Lanes {
   }
   __device__ __forceinline__ int min(int v) const { return __reduce_min_sync(m(), v); }
   __device__ __forceinline__ int max(int v) const { return __reduce_max_sync(m(), v); }
+  // 64-bit group min / max as two 32-bit redux.sync reductions: the high
+  // word, then the low word over the lanes tied on it (exact; replaces
+  // log2(W) rounds of paired 32-bit shuffles)
   __device__ __forceinline__ unsigned long long min_u64(unsigned long long v) const {
-#pragma unroll
-    for (int o = W >> 1; o > 0; o >>= 1) {
-      const unsigned long long w = shfl_xor(v, o);
-      v = w < v ? w : v;
-    }
-    return v;
+    const unsigned hi = (unsigned)(v >> 32);
+    const unsigned mh = __reduce_min_sync(m(), hi);
+    const unsigned ml = __reduce_min_sync(m(), hi == mh ? (unsigned)v : 0xffffffffu);
+    return ((unsigned long long)mh << 32) | ml;
   }
   __device__ __forceinline__ unsigned long long max_u64(unsigned long long v) const {
-#pragma unroll
-    for (int o = W >> 1; o > 0; o >>= 1) {
-      const unsigned long long w = shfl_xor(v, o);
-      v = w > v ? w : v;
-    }
-    return v;
+    const unsigned hi = (unsigned)(v >> 32);
+    const unsigned mh = __reduce_max_sync(m(), hi);
+    const unsigned ml = __reduce_max_sync(m(), hi == mh ? (unsigned)v : 0u);
+    return ((unsigned long long)mh << 32) | ml;
   }
   __device__ __forceinline__ long long sum_ll(long long v) const {
 #pragma unroll
