@@ -180,45 +180,89 @@ def agent_for(m):
     return dims, engine.mlp_random_init(dims, 42)
 
 
-def cpu_reference(cfgname, sample_replays, threads):
-    """Compiled unmodified reference (oracle/_ref) on host threads: a bounded
-    sample of the config's replays (for a sweep, spread over its policies
-    and arrival rates).  Returns (decisions/s, decisions, wall s, description)."""
+def ref_agent_for(m):
+    """The same agent from the compiled reference (DqnAgent ctor, dqn.hpp:60-65)."""
     sys.path.insert(0, str(ROOT / "tests"))
     import oracles as O  # baseline infrastructure
-    from paper_2408_13510_b200 import abi, engine
+    from paper_2408_13510_b200 import abi
+    sd = abi.state_dimension(m)
+    return [sd, 64, 64, m + 1], O.ref_agent_params(sd, m + 1, 64, 42)
+
+
+def sample_plan(cfgname, per):
+    """The bounded CPU sample of a config: per policy, `per` replays with
+    seeds 1..per and the sweep's arrival rates spread over them.  Returns
+    [(policy, [(rate_index, seed), ...])]; replay (rate_index, seed) is the
+    engine's replay rate_index * R + seed - 1 on rank 0 (make_workload)."""
+    n, R, m, rates, pols, weights, desc = cfg_shape(cfgname)
+    step = max(1, len(rates) // per)
+    return [(policy, [((pi + k * step) % len(rates), k + 1) for k in range(per)])
+            for pi, policy in enumerate(pols)]
+
+
+def cpu_reference(cfgname, sample_replays, threads):
+    """Compiled unmodified reference (oracle/_ref) on host threads over the
+    bounded sample of sample_plan: traces from the reference's own generator
+    (build_workload, experiment.hpp:291-305, via ref_generate_mixture), the
+    agent from its own DqnAgent constructor, replays through its own
+    ClusterSim::run_policy.  Nothing of the engine is loaded on this path.
+    Returns (decisions/s, decisions, wall s, description, samples) with
+    samples = [(policy, rate_index, seed, rs_replay_stats record)]."""
+    sys.path.insert(0, str(ROOT / "tests"))
+    import oracles as O  # baseline infrastructure
+    from paper_2408_13510_b200 import abi  # ctypes structs only (no library load)
     n, R, m, rates, pols, weights, desc = cfg_shape(cfgname)
     lib = O.ref_lib()
     per = max(1, sample_replays)  # one replay per host thread, per policy
     ticks = 0
     wall = 0.0
-    for pi, policy in enumerate(pols):
-        # this policy's sample: seeds 1..per, rates spread over the sweep
-        pick = [rates[(pi + k * max(1, len(rates) // per)) % len(rates)] for k in range(per)]
-        parts = [engine.build_workload([k + 1], n, rate, weights) for k, rate in enumerate(pick)]
-        tb = engine.TraceBatch(np.arange(per + 1, dtype=np.int64) * n,
-                               np.concatenate([t.arrival for t in parts]),
-                               np.concatenate([t.prompt for t in parts]),
-                               np.concatenate([t.decode for t in parts]),
-                               np.concatenate([t.task for t in parts]))
-        ps = np.array([abi.mix_seed(k + 1, 0x9DED) for k in range(per)], np.uint64)
+    samples = []
+    for policy, picks in sample_plan(cfgname, per):
+        traces = [O.ref_generate(seed, n, rates[ri], weights) for ri, seed in picks]
+        off = np.arange(per + 1, dtype=np.int64) * n
+        cat = lambda f: np.ascontiguousarray(np.concatenate([getattr(t, f) for t in traces]))
+        arr, pr, de, tk = cat("arrival"), cat("prompt"), cat("decode"), cat("task")
+        ps = np.array([O.ref_lib().ref_mix_seed(seed, 0x9DED) for _, seed in picks], np.uint64)
         cfg = abi.default_config(policy, m)
         keep = None
         if policy == "rl":
-            dims, params = agent_for(m)
+            dims, params = ref_agent_for(m)
             keep = abi.set_rl(cfg, dims, params)
         stats = np.zeros(per, abi.STATS_DTYPE)
-        w = lib.ref_run_batch(C.byref(cfg), per, tb.offsets.ctypes.data, tb.arrival.ctypes.data,
-                              tb.prompt.ctypes.data, tb.decode.ctypes.data, tb.task.ctypes.data,
+        w = lib.ref_run_batch(C.byref(cfg), per, off.ctypes.data, arr.ctypes.data,
+                              pr.ctypes.data, de.ctypes.data, tk.ctypes.data,
                               ps.ctypes.data, None, threads, stats.ctypes.data)
         del keep
         if w <= 0:
             raise RuntimeError("reference batch failed: " + O.ref_error())
         ticks += int(stats["ticks"].sum())
         wall += w
+        samples += [(policy, ri, seed, stats[k]) for k, (ri, seed) in enumerate(picks)]
     what = (f"{per} replays (seeds 1..{per}) per policy x {len(pols)} "
             f"{'policies' if len(pols) > 1 else 'policy'} of the {cfgname} workload")
-    return ticks / wall, ticks, wall, what
+    return ticks / wall, ticks, wall, what, samples
+
+
+# rs_replay_stats fields the reference's run_policy + compute_metrics sums
+# define without a trajectory (ref_run_batch records none): compared exactly
+PARITY_FIELDS = ("decision_hash", "ticks", "routed", "infeasible", "completed", "status",
+                 "total_preemptions", "total_tokens", "tbt_count", "clock", "total_e2e_s",
+                 "total_ttft_s", "total_tbt_s", "total_router_wait_s", "makespan_s")
+
+
+def parity_sample(cfgname, samples, cell_stats, pols, R):
+    """The engine's own answers for the replays the reference just ran on the
+    host, field by field (bitwise for the fp64 sums): the bench checks itself."""
+    bad = []
+    for policy, ri, seed, want in samples:
+        got = cell_stats[pols.index(policy)][ri * R + seed - 1]
+        diff = [f for f in PARITY_FIELDS
+                if np.asarray(got[f]).tobytes() != np.asarray(want[f]).tobytes()]
+        if diff:
+            bad.append({"policy": policy, "rate_index": ri, "seed": seed, "fields": diff})
+    return {"checked": len(samples), "bit_exact": len(samples) - len(bad),
+            "against": "oracle/_ref (compiled unmodified reference, same seeds)",
+            "fields": list(PARITY_FIELDS), "mismatches": bad[:8]}
 
 
 def cpu_port_scan_free(cfgname, sample_replays, threads):
@@ -229,26 +273,23 @@ def cpu_port_scan_free(cfgname, sample_replays, threads):
     from concurrent.futures import ThreadPoolExecutor
     sys.path.insert(0, str(ROOT / "tests"))
     import oracles as O  # baseline infrastructure
-    from paper_2408_13510_b200 import abi, engine
+    from paper_2408_13510_b200 import abi
     n, R, m, rates, pols, weights, desc = cfg_shape(cfgname)
     per = max(1, sample_replays)
     ticks = 0
     wall = 0.0
-    for pi, policy in enumerate(pols):
-        pick = [rates[(pi + k * max(1, len(rates) // per)) % len(rates)] for k in range(per)]
-        traces = []
-        for k, rate in enumerate(pick):
-            t = engine.build_workload([k + 1], n, rate, weights)
-            traces.append(O.Trace(t.arrival, t.prompt, t.decode, t.task))
+    for policy, picks in sample_plan(cfgname, per):
+        traces = [O.ref_generate(seed, n, rates[ri], weights) for ri, seed in picks]
         cfg = abi.default_config(policy, m)
         keep = None
         if policy == "rl":
-            dims, params = agent_for(m)
+            dims, params = ref_agent_for(m)
             keep = abi.set_rl(cfg, dims, params)
         O.ora_lib()
         t0 = time.perf_counter()
         with ThreadPoolExecutor(threads) as ex:  # ctypes releases the GIL
-            res = list(ex.map(lambda k: O.ora_run(cfg, traces[k], abi.mix_seed(k + 1, 0x9DED)),
+            res = list(ex.map(lambda k: O.ora_run(cfg, traces[k],
+                                                  abi.mix_seed(picks[k][1], 0x9DED)),
                               range(per)))
         wall += time.perf_counter() - t0
         ticks += sum(int(r.stats["ticks"][0]) for r in res)
@@ -256,31 +297,58 @@ def cpu_port_scan_free(cfgname, sample_replays, threads):
     return ticks / wall, ticks, wall
 
 
+def config_dict(cfgname, world):
+    """The workload description both arms print (same keys, same values)."""
+    n, R, m, rates, pols, weights, desc = cfg_shape(cfgname)
+    rate_s = (f"{rates[0]:g}" if len(rates) == 1 else f"{rates[0]:g}..{rates[-1]:g} "
+              f"({len(rates)} rates)")
+    return {"workload": desc, "policy": "+".join(pols), "instances": m,
+            "requests_per_replay": n, "replays_per_gpu": R * len(rates) * len(pols),
+            "arrival_rate": rate_s, "predictor": "simulated, Table-1 accuracy",
+            "l2": f"inputs {(8 + 4 + 4 + 1) * n * R * len(rates) / 1e6:.0f} MB per GPU "
+                  f"{'>' if (8 + 4 + 4 + 1) * n * R * len(rates) > 126e6 else '<='} 126 MB L2 "
+                  "(no flush between steps)",
+            "parallelism": f"replay shards x{world} (weak)"}
+
+
 def run_reference_impl(args, cfgname):
     rank, world, _ = dist_env()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n, R, m, rates, pols, weights, desc = cfg_shape(cfgname)
-    sample = threads
+    sample = min(threads, 64, cfg_shape(cfgname)[1])
     runs = []
     for i in range(args.warmup + args.steps):
-        v, ticks, wall, what = cpu_reference(cfgname, sample, threads)
+        v, ticks, wall, what, _ = cpu_reference(cfgname, sample, threads)
         if i >= args.warmup:
             runs.append((v, wall))
     value = float(np.mean([r[0] for r in runs]))
+    config = config_dict(cfgname, args.gpus)
+    config["sample_replays"] = f"{what} per step (bounded sample, same seeds every step)"
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": float(np.mean([r[1] for r in runs]) * 1e3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (reference workload generator)",
-            "config": {"workload": desc, "policy": "+".join(pols), "instances": m,
-                       "requests_per_replay": n},
+            "data": "synthetic (reference workload generator, oracle/_ref)",
+            "config": config,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"{what}, one replay per host thread, per step"},
+                             "sample": f"{what}, on {threads} host threads, per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one per GPU) on
+    this node the way the driver does, and return their exit code."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -298,9 +366,13 @@ def main():
         n, R, m, rate, pol, w, desc = CONFIGS[args.config]
         CONFIGS[args.config] = (n, args.replays, m, rate, pol, w,
                                 desc.replace(f"{R:,}", f"{args.replays:,}"))
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
     if args.impl == "reference":
         run_reference_impl(args, args.config)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
 
     import torch
     import torch.distributed as dist
@@ -308,6 +380,10 @@ def main():
     from paper_2408_13510_b200 import dist as rdist
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: one rank per GPU")
+    if not os.environ.get("RS_BENCH_SAME_DEVICE") and torch.cuda.device_count() < world:
+        raise SystemExit(f"--gpus {world}: only {torch.cuda.device_count()} visible GPUs")
     # RS_BENCH_SAME_DEVICE / RS_DIST_BACKEND=gloo exist only to exercise the
     # multi-rank path on a one-GPU box; the real run is one rank per GPU on NCCL.
     if os.environ.get("RS_BENCH_SAME_DEVICE"):
@@ -517,22 +593,15 @@ def main():
                 traffic = pj.get("dram_bytes_per_launch")
         except (ValueError, OSError):
             traffic = None
-    rate_s = (f"{rates[0]:g}" if len(rates) == 1 else f"{rates[0]:g}..{rates[-1]:g} "
-              f"({len(rates)} rates)")
+    config = config_dict(args.config, world)
+    config["prewarm_s"] = PREWARM_S
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed * 1e3 / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic: reference workload generator, seeds 1..{R_seeds * world} "
                 f"(rank r takes seeds r*{R_seeds}+1..(r+1)*{R_seeds})",
-        "config": {"workload": desc, "policy": "+".join(pols), "instances": m,
-                   "requests_per_replay": n, "replays_per_gpu": R * len(cells),
-                   "arrival_rate": rate_s,
-                   "predictor": "simulated, Table-1 accuracy",
-                   "l2": f"inputs {(8 + 4 + 4 + 1) * N / 1e6:.0f} MB per GPU > 126 MB L2 "
-                         "(no flush needed)",
-                   "parallelism": f"replay shards x{world} (weak)",
-                   "prewarm_s": PREWARM_S},
+        "config": config,
         "decisions_per_step": ticks_total, "unfinished_replays": unfinished,
         "gpu_launches": 3 * len(cells) * args.steps * world,  # validate + replay + stats
         "kernel_ms": {"replay_batch": replay_s * 1e3, "per_step": step_ms},
@@ -578,26 +647,34 @@ def main():
                               for c, st, ms in zip(cells, cell_stats, cell_ms)}
     if e2e:
         line["e2e"] = e2e
-    if world == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        sample = min(threads, 64, R_seeds)
         try:
-            threads = os.cpu_count() or 1
-            sample = min(threads, 64)
-            cv, cticks, cwall, what = cpu_reference(args.config, sample, threads)
-            line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": min(threads, sample),
-                                    "kind": "reference",
-                                    "sample": f"{what} on {min(threads, sample)} host threads, "
-                                              f"{cwall:.1f} s wall, {cticks} decisions"}
+            cv, cticks, cwall, what, samples = cpu_reference(args.config, sample, threads)
+            # the bench checks its own answers: the engine's stats for the
+            # replays the reference just ran, compared field by field
+            line["parity_sample"] = parity_sample(args.config, samples, cell_stats, list(pols),
+                                                  R_seeds)
+            if world == 1:  # the reported CPU baseline: rank 0 at N = 1 only
+                line["cpu_baseline"] = {"value": cv, "unit": UNIT, "cores": threads,
+                                        "kind": "reference",
+                                        "sample": f"{what} on {threads} host threads, "
+                                                  f"{cwall:.1f} s wall, {cticks} decisions"}
         except Exception as e:  # baseline is reported, never the target
-            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
-                                    "sample": f"unavailable: {e}"}
-        try:
-            pv, pticks, pwall = cpu_port_scan_free(args.config, sample, threads)
-            line["cpu_baseline_scan_free"] = {
-                "value": pv, "unit": UNIT, "cores": min(threads, sample), "kind": "port",
-                "sample": f"same sample, oracle/rs_oracle.c (no per-tick reward scan), "
-                          f"{pwall:.1f} s wall, {pticks} decisions"}
-        except Exception as e:
-            line["cpu_baseline_scan_free"] = {"value": None, "sample": f"unavailable: {e}"}
+            line["parity_sample"] = {"checked": 0, "bit_exact": 0, "error": str(e)}
+            if world == 1:
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0,
+                                        "kind": "reference", "sample": f"unavailable: {e}"}
+        if world == 1:
+            try:
+                pv, pticks, pwall = cpu_port_scan_free(args.config, sample, threads)
+                line["cpu_baseline_scan_free"] = {
+                    "value": pv, "unit": UNIT, "cores": threads, "kind": "port",
+                    "sample": f"same sample, oracle/rs_oracle.c (no per-tick reward scan), "
+                              f"{pwall:.1f} s wall, {pticks} decisions"}
+            except Exception as e:
+                line["cpu_baseline_scan_free"] = {"value": None, "sample": f"unavailable: {e}"}
     print(json.dumps(line), flush=True)
     del keep
     if world > 1:
