@@ -361,6 +361,9 @@ def main():
     ap.add_argument("--replays", type=int, default=0, help="override seeds per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dump-stats", default="",
+                    help="rank 0 saves every rank's per-replay stats (the gathered records) "
+                         "of the first cell as .npy (tests)")
     args = ap.parse_args()
     if args.replays:
         n, R, m, rate, pol, w, desc = CONFIGS[args.config]
@@ -575,6 +578,11 @@ def main():
             if not np.array_equal(h_stats["decision_hash"], st["decision_hash"]):
                 raise RuntimeError("e2e path decisions differ from the device path")
 
+    if args.dump_stats:  # every rank's records of the first cell, in rank order
+        src = cells[0]["st"] if backend == "nccl" else cells[0]["st"].cpu()
+        allst = rdist.gather_stats(src, world) if world > 1 else src
+        if rank == 0:
+            np.save(args.dump_stats, rdist.stats_view(allst))
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()

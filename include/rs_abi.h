@@ -330,6 +330,20 @@ rs_status rs_replay_batch_host(const rs_batch_cfg* cfg, const rs_trace_soa* trac
                                rs_req_out* out, rs_replay_stats* stats,
                                int32_t device);
 
+/* rs_replay_batch_host sharded over several devices of this process
+ * (evaluate_policy's independent seed loop,
+ * experiment.hpp:648-670, run concurrently as SPEC.md:523-524 allows):
+ * replays [k*S, (k+1)*S), S = ceil(num_replays / ndev), run on devices[k],
+ * each device on its own stream and host thread with no collective on the
+ * data path; the per-replay statistics are then all-gathered over NCCL
+ * (ncclCommInitAll over `devices`, libnccl.so.2 opened at first use) and
+ * copied to `stats` from devices[0].  Results are identical to one
+ * rs_replay_batch_host call over the whole batch.  `devices` must be
+ * distinct; RS_ERR_UNSUPPORTED when NCCL cannot be loaded. */
+rs_status rs_replay_batch_multi(const rs_batch_cfg* cfg, const rs_trace_soa* trace,
+                                rs_req_out* out, rs_replay_stats* stats,
+                                const int32_t* devices, int32_t ndev);
+
 /* rs_replay_trajectory with host buffers (trace, outputs and the
  * trajectory arrays in `traj`), on `device`; the reference-facing form of
  * ClusterSim::trajectory() (env.hpp:203) for a batch. */

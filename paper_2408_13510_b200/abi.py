@@ -345,7 +345,7 @@ EXPORTED_SYMBOLS = (
     "rs_heavy_decode_cutoff", "rs_host_alloc", "rs_host_free", "rs_mlp_random_init",
     "rs_replay_trajectory", "rs_replay_trajectory_host", "rs_emit_report",
     "rs_dqn_workspace_size", "rs_dqn_update", "rs_dqn_update_host",
-    "rs_empirical_fit", "rs_empirical_fit_trace",
+    "rs_empirical_fit", "rs_empirical_fit_trace", "rs_replay_batch_multi",
 )
 
 
@@ -362,6 +362,8 @@ def _declare(lib: C.CDLL) -> None:
                                     C.c_void_p, C.c_size_t, C.c_void_p]
     lib.rs_replay_batch_host.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,
                                          C.c_int32]
+    lib.rs_replay_batch_multi.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,
+                                          C.c_void_p, C.c_int32]
     lib.rs_replay_trajectory.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,
                                          P(Trajectory), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.rs_replay_trajectory_host.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,

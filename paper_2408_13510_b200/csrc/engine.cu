@@ -822,12 +822,17 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
       pl.kern = lat;
     cudaGetLastError();
   }
-  if (env_int("RS_DEBUG_PLAN", 0))
+  if (env_int("RS_DEBUG_PLAN", 0)) {
+    const char* variant = !fast                                                ? "general"
+                          : pl.kern == kernel_for(cfg->policy, fast, groups, pl.width, 2) ? "lat"
+                          : pl.kern == kernel_for(cfg->policy, fast, groups, pl.width, 1) ? "wide"
+                                                                                        : "bounded";
     fprintf(stderr,
-            "rs plan: policy %d fast %d groups %d width %d wpb %d blocks/SM %d block_smem %d "
-            "group_bytes %d weights %d resident replays %lld\n",
-            cfg->policy, (int)fast, groups, pl.width, pl.wpb, pl.per_sm, pl.block_smem,
-            L.group_bytes, L.weights_bytes, pl.capacity);
+            "rs plan: policy %d fast %d kernel %s groups %d width %d wpb %d blocks/SM %d "
+            "block_smem %d group_bytes %d weights %d wcap %d rl_global %d resident replays %lld\n",
+            cfg->policy, (int)fast, variant, groups, pl.width, pl.wpb, pl.per_sm, pl.block_smem,
+            L.group_bytes, L.weights_bytes, L.wcap, (int)rl_global, pl.capacity);
+  }
   RS_CUDA(cudaMemsetAsync(kp.work_counter, 0, sizeof(int), st));
   if (fast && !resident && env_int("RS_NO_VALIDATE_PASS", 0) == 0) {
     // resident inputs: validation + preemption-counter zeroing as one

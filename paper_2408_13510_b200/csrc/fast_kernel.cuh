@@ -732,12 +732,11 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
       // instances emptied by this tick's last events skip ahead (instance.hpp:309)
       if (S[g].clock < t1 && S[g].n == 0 && S[g].w_cnt == 0) S[g].clock = t1;
     }
-    // one reduction: completions (low 16 bits) + biased waiting deltas
+    // completions and waiting-count changes of the tick (two exact sums: a
+    // large delta_t can admit or preempt any number of requests in one tick)
     if (L.any((comps | wdelta) != 0)) {
-      const unsigned packed =
-          L.sum((int)((unsigned)comps | ((unsigned)(wdelta + 1024) << 16)));
-      R.completed += (int)(packed & 0xffffu);
-      R.total_wait += (int)(packed >> 16) - W * 1024;
+      R.completed += L.sum(comps);
+      R.total_wait += L.sum(wdelta);
     }
     R.clock = t1;
     if (R.clock >= R.next_arr) {  // inject_arrivals (env.hpp:357-375) only when due

@@ -39,6 +39,18 @@ rs_status fail2(rs_status s, const std::string& m) {
 
 size_t al(size_t v) { return (v + 255) / 256 * 256; }
 
+// A captured rs_replay_batch_host call.  The graph's watermark copies read
+// `marks` when the graph runs, so every graph owns its pinned values, written
+// once at capture and never again (a later call of another shape cannot
+// change what a replayed graph streams).
+struct GraphEntry {
+  std::vector<char> key;  // call shape and every pointer the graph bakes in
+  cudaGraphExec_t exec = nullptr;
+  int* marks = nullptr;
+  uint64_t used = 0;
+};
+constexpr int kMaxGraphs = 8;  // e.g. the four policy cells of c4, alternating
+
 // Per-device cached arena + stream for the host entry points.
 struct DeviceCache {
   std::mutex mu;
@@ -47,17 +59,28 @@ struct DeviceCache {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;      // streamed inputs (rs_replay_batch_host)
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
-  int* marks = nullptr;                    // pinned residency watermarks
+  int* marks = nullptr;                    // pinned watermarks of direct (uncaptured) calls
   int nmarks = 0;
-  cudaGraphExec_t gexec = nullptr;         // captured rs_replay_batch_host call
-  std::vector<char> gkey, warm_key;        // its shape / pointers; the last uncaptured call
+  std::vector<GraphEntry> graphs;          // LRU, <= kMaxGraphs
+  std::vector<std::vector<char>> warm;     // recent uncaptured keys: captured on a repeat
+  uint64_t tick = 0;
 };
 DeviceCache g_cache[16];
+
+void drop_graphs(DeviceCache& c) {
+  for (GraphEntry& g : c.graphs) {
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (g.marks) cudaFreeHost(g.marks);
+  }
+  c.graphs.clear();
+  c.warm.clear();
+}
 
 rs_status arena(int dev, size_t need, char** out, cudaStream_t* st) {
   DeviceCache& c = g_cache[dev];
   if (!c.stream) RS_CUDA2(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
   if (c.bytes < need) {
+    drop_graphs(c);  // captured calls point into the old arena
     if (c.base) cudaFree(c.base);
     c.base = nullptr;
     c.bytes = 0;
@@ -231,8 +254,20 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
   // work per call instead of ~3 ms of copy / launch calls, so a host-side
   // stall (the host thread descheduled mid-enqueue, measured at up to 0.2 s
   // on a shared box) no longer delays the device work.
+  // chunk boundaries of the streamed inputs: a small first chunk (the
+  // kernel starts on it), then x8 (each chunk lands well before the replays
+  // consume the previous one; few chunks = few 2D copy commands to queue)
+  std::vector<int> bounds;
+  if (stream_in) {
+    for (int64_t e = std::min<int64_t>(n_eq, 256); ; e = std::min<int64_t>(n_eq, 8 * e)) {
+      bounds.push_back((int)e);
+      if (e == n_eq) break;
+    }
+  }
   auto w1 = w0;
-  auto enqueue = [&]() -> rs_status {
+  // `marks`: pinned watermark values (bounds) the copy stream raises; owned
+  // by the graph being captured, or the scratch of a direct call
+  auto enqueue = [&](int* marks) -> rs_status {
     RS_CUDA2(h2d(o_off, tr->offsets, 8ull * (R + 1)));
     if (!stream_in) {
       RS_CUDA2(h2d(o_arr, tr->arrival_s, 8ull * N));
@@ -283,26 +318,10 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
           RS_OK)
         return s;
     } else {
-      // chunk boundaries: a small first chunk (the kernel starts on it), then
-      // x8 (each chunk lands well before the replays consume the previous one;
-      // few chunks = few 2D copy commands to queue)
-      std::vector<int> bounds;
-      for (int64_t e = std::min<int64_t>(n_eq, 256); ; e = std::min<int64_t>(n_eq, 8 * e)) {
-        bounds.push_back((int)e);
-        if (e == n_eq) break;
-      }
       if (!dc.copy_stream)
         RS_CUDA2(cudaStreamCreateWithFlags(&dc.copy_stream, cudaStreamNonBlocking));
       if (!dc.ev_ready) RS_CUDA2(cudaEventCreateWithFlags(&dc.ev_ready, cudaEventDisableTiming));
       if (!dc.ev_done) RS_CUDA2(cudaEventCreateWithFlags(&dc.ev_done, cudaEventDisableTiming));
-      if (dc.nmarks < (int)bounds.size()) {
-        if (dc.marks) cudaFreeHost(dc.marks);
-        dc.marks = nullptr;
-        dc.nmarks = 0;
-        RS_CUDA2(cudaMallocHost(&dc.marks, sizeof(int) * bounds.size()));
-        dc.nmarks = (int)bounds.size();
-      }
-      for (size_t i = 0; i < bounds.size(); ++i) dc.marks[i] = bounds[i];
       int* flag = reinterpret_cast<int*>(b + o_fl);
       RS_CUDA2(cudaMemsetAsync(flag, 0, sizeof(int), st));
       RS_CUDA2(cudaEventRecord(dc.ev_ready, st));
@@ -329,7 +348,7 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
                                      (size_t)(hi - lo) * c.es, (size_t)R, cudaMemcpyHostToDevice,
                                      cs));
         }
-        RS_CUDA2(cudaMemcpyAsync(flag, dc.marks + i, sizeof(int), cudaMemcpyHostToDevice, cs));
+        RS_CUDA2(cudaMemcpyAsync(flag, marks + i, sizeof(int), cudaMemcpyHostToDevice, cs));
         lo = hi;
       }
       RS_CUDA2(cudaEventRecord(dc.ev_done, cs));
@@ -392,41 +411,66 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
       put(&o, sizeof(o));
       put(&n_eq, sizeof(n_eq));
       put(&stream_in, sizeof(stream_in));
-      if (dc.gexec && key == dc.gkey) {
-        RS_CUDA2(cudaGraphLaunch(dc.gexec, st));
+      GraphEntry* hit = nullptr;
+      for (GraphEntry& g : dc.graphs)
+        if (g.key == key) hit = &g;
+      auto wit = std::find(dc.warm.begin(), dc.warm.end(), key);
+      if (hit) {
+        hit->used = ++dc.tick;
+        RS_CUDA2(cudaGraphLaunch(hit->exec, st));
         graphed = true;
-      } else if (key == dc.warm_key) {  // second identical call: capture
-        if (dc.gexec) {
-          cudaGraphExecDestroy(dc.gexec);
-          dc.gexec = nullptr;
-          dc.gkey.clear();
+      } else if (wit != dc.warm.end()) {  // second identical call: capture
+        dc.warm.erase(wit);
+        if ((int)dc.graphs.size() >= kMaxGraphs) {  // evict the least recently used
+          auto lru = std::min_element(dc.graphs.begin(), dc.graphs.end(),
+                                      [](const GraphEntry& a, const GraphEntry& b) {
+                                        return a.used < b.used;
+                                      });
+          if (lru->exec) cudaGraphExecDestroy(lru->exec);
+          if (lru->marks) cudaFreeHost(lru->marks);
+          dc.graphs.erase(lru);
+        }
+        GraphEntry e;
+        e.key = key;
+        e.used = ++dc.tick;
+        if (!bounds.empty()) {
+          RS_CUDA2(cudaMallocHost(&e.marks, sizeof(int) * bounds.size()));
+          std::copy(bounds.begin(), bounds.end(), e.marks);
         }
         cudaGraph_t g = nullptr;
         if (cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) == cudaSuccess) {
-          const rs_status cs_ = enqueue();
+          const rs_status cs_ = enqueue(e.marks);
           const cudaError_t ce = cudaStreamEndCapture(st, &g);
           if (cs_ == RS_OK && ce == cudaSuccess && g &&
-              cudaGraphInstantiate(&dc.gexec, g, 0) == cudaSuccess) {
-            dc.gkey = key;
-            graphed = cudaGraphLaunch(dc.gexec, st) == cudaSuccess;
+              cudaGraphInstantiate(&e.exec, g, 0) == cudaSuccess &&
+              cudaGraphLaunch(e.exec, st) == cudaSuccess) {
+            graphed = true;
+            dc.graphs.push_back(e);
           }
           if (g) cudaGraphDestroy(g);
-          if (!graphed) {  // fall back to direct enqueue
-            cudaGetLastError();
-            if (dc.gexec) cudaGraphExecDestroy(dc.gexec);
-            dc.gexec = nullptr;
-            dc.gkey.clear();
-            dc.warm_key.clear();
-          }
-        } else {
+        }
+        if (!graphed) {  // fall back to a direct enqueue
           cudaGetLastError();
+          if (e.exec) cudaGraphExecDestroy(e.exec);
+          if (e.marks) cudaFreeHost(e.marks);
         }
       } else {
-        dc.warm_key = key;
+        if ((int)dc.warm.size() >= kMaxGraphs) dc.warm.erase(dc.warm.begin());
+        dc.warm.push_back(key);
       }
     }
   }
-  if (!graphed && (s = enqueue()) != RS_OK) return s;
+  if (!graphed) {
+    if (dc.nmarks < (int)bounds.size()) {
+      if (dc.marks) cudaFreeHost(dc.marks);
+      dc.marks = nullptr;
+      dc.nmarks = 0;
+      RS_CUDA2(cudaMallocHost(&dc.marks, sizeof(int) * bounds.size()));
+      dc.nmarks = (int)bounds.size();
+    }
+    std::copy(bounds.begin(), bounds.end(), dc.marks);
+    if ((s = enqueue(dc.marks)) != RS_OK) return s;
+  }
   if (dbg) cudaEventRecord(tev[2], st);
   RS_CUDA2(cudaStreamSynchronize(st));
   if (dbg) {
