@@ -115,11 +115,16 @@ struct KParams {
   int f_rreq, f_rprompt, f_rdhat, f_rtrue, f_rkey;
   int f_wreq, f_wprompt, f_wdhat, f_wtrue, f_wemit;
   int rstride, mwidth;
+  // Running entries j < rsm of an instance live in shared memory; entries
+  // j >= rsm (a batch larger than the shared head: rare) in a per-warp
+  // global tail of m x rtail slots per field (L2-resident), so large fleets
+  // keep several replays resident per SM (rsm = rcap: no tail)
+  int rsm, rtail;
+  int* run_tail;
   // Divisors that are exact powers of two divide by an exact reciprocal
   // multiply (IEEE scaling: bit-identical to the division).
   double inv_eps, inv_kv, inv_mb;
   int eps_pow2, kv_pow2, mb_pow2;
-  int ub_max;  // largest upper_bound_tokens (32-bit aggregate guard)
   // fused predictor (fast kernel): predictions drawn at arrival injection
   int predict_inline;
   int off_pred;                    // mt19937_64 state + 312 outputs (bytes)
@@ -131,7 +136,7 @@ struct KParams {
   const int* resident;
   // ClusterConfig::record_trajectory (general kernel only): per-tick reward
   // (env.hpp:257-303) and TickRecords (env.hpp:305-319)
-  const int2* vinfo;    // fast kernel: per-replay {bad, vmax} from validate_kernel (null: walk the trace)
+  const int2* vinfo;    // fast kernel: per-replay {bad, 0} from validate_kernel (null: walk the trace)
   rs_trajectory traj;   // device arrays (by value); traj_on = 0: off
   int traj_on;
   double r_w, c_k;      // RewardConfig::r_w, shaping_coefficient(episode_k)

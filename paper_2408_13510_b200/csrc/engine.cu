@@ -66,7 +66,7 @@ rs_status require_device() {
 
 // Smem layout of one replay group (one warp) for this config.
 struct Layout {
-  int rcap, wcap;
+  int rcap, rsm, wcap;
   int off_run, off_wait, off_dbc, off_rlx, off_rng, off_front, off_pred, group_bytes;
   int weights_bytes;
   int woff[RS_MAX_LAYERS], boff[RS_MAX_LAYERS];
@@ -79,17 +79,25 @@ int min_reservation(const rs_batch_cfg& c) {
   return (int)std::max<int64_t>(2, 1 + mn);
 }
 
+int run_cap(const rs_batch_cfg& c) {
+  const int rcap =
+      (int)std::min<int64_t>(c.max_batch_size, c.kv_capacity_tokens / min_reservation(c));
+  return std::max(rcap, 1);
+}
+
 // fast = the lane-per-instance kernel (no InstHot block, 5 running fields
-// with an odd per-instance stride so lane-owned rows hit distinct banks).
-Layout make_layout(const rs_batch_cfg& c, int wcap, bool fast) {
+// with an odd per-instance stride so lane-owned rows hit distinct banks;
+// the first rsm entries of each instance in shared memory, the rest in the
+// warp's global tail).
+Layout make_layout(const rs_batch_cfg& c, int wcap, bool fast, int rsm = 0) {
   Layout L{};
   const int m = c.num_instances;
-  L.rcap = (int)std::min<int64_t>(c.max_batch_size, c.kv_capacity_tokens / min_reservation(c));
-  if (L.rcap < 1) L.rcap = 1;
+  L.rcap = run_cap(c);
+  L.rsm = fast ? std::max(1, std::min(rsm > 0 ? rsm : L.rcap, L.rcap)) : L.rcap;
   L.wcap = wcap;
   size_t off = fast ? 0 : (size_t)m * sizeof(rs::InstHot);
   L.off_run = (int)off;
-  off = fast ? align_up(off + 5ull * m * (L.rcap | 1) * sizeof(int), 16)
+  off = fast ? align_up(off + 5ull * m * (L.rsm | 1) * sizeof(int), 16)
              : align_up(off + 6ull * m * L.rcap * sizeof(int), 16);
   L.off_wait = (int)off;
   off = align_up(off + 5ull * m * L.wcap * sizeof(int), 16);
@@ -213,8 +221,30 @@ int64_t heavy_cutoff(const rs_profile& p, const rs_thresholds& t) {
 }
 
 struct WsLayout {
-  size_t counter, next, prev, emit, removed, wt, vinfo, total;
+  size_t counter, next, prev, emit, removed, wt, vinfo, tail, total;
 };
+
+int sm_count() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) {
+    cudaGetLastError();
+    return 148;  // B200
+  }
+  return sms;
+}
+
+// Global tails of the fast kernel's running entries: every warp that can be
+// resident (<= 64 per SM) owns 5 fields x m instances x
+// (rcap - 1) slots (the smallest shared head is one entry).
+size_t run_tail_ints(const rs_batch_cfg& c, int64_t num_replays) {
+  const int rcap = run_cap(c);
+  if (c.chunk_size != 0 || c.num_instances > 64 || rcap <= 1) return 0;
+  // (a launch may round the replay count up to whole blocks of <= 16 warps,
+  // and any warp can take any replay from the work counter)
+  const int64_t warps = std::min<int64_t>(num_replays + 16, (int64_t)sm_count() * 64);
+  return (size_t)warps * 5 * c.num_instances * (rcap - 1);
+}
 
 size_t rl_param_count(const rs_batch_cfg& c) {
   if (c.policy != RS_POLICY_RL) return 0;
@@ -224,7 +254,8 @@ size_t rl_param_count(const rs_batch_cfg& c) {
   return w;
 }
 
-WsLayout ws_layout(int64_t total_requests, int64_t num_replays, size_t rl_params = 0) {
+WsLayout ws_layout(int64_t total_requests, int64_t num_replays, size_t rl_params = 0,
+                   size_t tail_ints = 0) {
   WsLayout w;
   size_t off = 0;
   w.wt = off;  // transposed Q-network (global-weights mode), may be empty
@@ -241,6 +272,8 @@ WsLayout ws_layout(int64_t total_requests, int64_t num_replays, size_t rl_params
   off = align_up(off + (size_t)total_requests, 256);
   w.vinfo = off;
   off = align_up(off + 8ull * (size_t)num_replays, 256);
+  w.tail = off;
+  off = align_up(off + 4ull * tail_ints, 256);
   w.total = off;
   return w;
 }
@@ -275,30 +308,49 @@ using KernelFn = void (*)(rs::KParams);
 // parallel) instantiates that policy's general and fast replay kernels.
 namespace rs {
 using KernelFn = void (*)(KParams);
-KernelFn kernel_for_0(bool fast, int groups, int width, int variant);
-KernelFn kernel_for_1(bool fast, int groups, int width, int variant);
-KernelFn kernel_for_2(bool fast, int groups, int width, int variant);
-KernelFn kernel_for_3(bool fast, int groups, int width, int variant);
-KernelFn kernel_for_4(bool fast, int groups, int width, int variant);
-KernelFn kernel_for_5(bool fast, int groups, int width, int variant);
-KernelFn kernel_for_6(bool fast, int groups, int width, int variant);
-KernelFn kernel_for_7(bool fast, int groups, int width, int variant);
-KernelFn kernel_for_8(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_0_0(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_0_1(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_1_0(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_1_1(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_2_0(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_2_1(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_3_0(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_3_1(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_4_0(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_4_1(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_5_0(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_5_1(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_6_0(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_6_1(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_7_0(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_7_1(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_8_0(bool fast, int groups, int width, int variant);
+KernelFn kernel_for_8_1(bool fast, int groups, int width, int variant);
 }  // namespace rs
 
 namespace {
 
-KernelFn kernel_for(int policy, bool fast, int groups, int width, int variant = 0) {
-  switch (policy) {
-    case 0: return rs::kernel_for_0(fast, groups, width, variant);
-    case 1: return rs::kernel_for_1(fast, groups, width, variant);
-    case 2: return rs::kernel_for_2(fast, groups, width, variant);
-    case 3: return rs::kernel_for_3(fast, groups, width, variant);
-    case 4: return rs::kernel_for_4(fast, groups, width, variant);
-    case 5: return rs::kernel_for_5(fast, groups, width, variant);
-    case 6: return rs::kernel_for_6(fast, groups, width, variant);
-    case 7: return rs::kernel_for_7(fast, groups, width, variant);
-    case 8: return rs::kernel_for_8(fast, groups, width, variant);
+KernelFn kernel_for(int policy, bool fast, int groups, int width, int variant = 0,
+                    bool tail = false) {
+  switch (policy * 2 + (tail ? 1 : 0)) {
+    case 0: return rs::kernel_for_0_0(fast, groups, width, variant);
+    case 1: return rs::kernel_for_0_1(fast, groups, width, variant);
+    case 2: return rs::kernel_for_1_0(fast, groups, width, variant);
+    case 3: return rs::kernel_for_1_1(fast, groups, width, variant);
+    case 4: return rs::kernel_for_2_0(fast, groups, width, variant);
+    case 5: return rs::kernel_for_2_1(fast, groups, width, variant);
+    case 6: return rs::kernel_for_3_0(fast, groups, width, variant);
+    case 7: return rs::kernel_for_3_1(fast, groups, width, variant);
+    case 8: return rs::kernel_for_4_0(fast, groups, width, variant);
+    case 9: return rs::kernel_for_4_1(fast, groups, width, variant);
+    case 10: return rs::kernel_for_5_0(fast, groups, width, variant);
+    case 11: return rs::kernel_for_5_1(fast, groups, width, variant);
+    case 12: return rs::kernel_for_6_0(fast, groups, width, variant);
+    case 13: return rs::kernel_for_6_1(fast, groups, width, variant);
+    case 14: return rs::kernel_for_7_0(fast, groups, width, variant);
+    case 15: return rs::kernel_for_7_1(fast, groups, width, variant);
+    case 16: return rs::kernel_for_8_0(fast, groups, width, variant);
+    case 17: return rs::kernel_for_8_1(fast, groups, width, variant);
   }
   return nullptr;
 }
@@ -381,7 +433,8 @@ rs_status rs_workspace_size(const rs_batch_cfg* cfg, int32_t num_replays,
   if (s != RS_OK) return s;
   if (!bytes || num_replays < 0 || total_requests < 0)
     return fail(RS_ERR_INVALID_ARGUMENT, "bad workspace query");
-  *bytes = ws_layout(total_requests, num_replays, rl_param_count(*cfg)).total;
+  *bytes = ws_layout(total_requests, num_replays, rl_param_count(*cfg),
+                     run_tail_ints(*cfg, num_replays)).total;
   return RS_OK;
 }
 
@@ -491,7 +544,8 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     return fail(RS_ERR_INVALID_ARGUMENT, "rs_replay_batch needs every per-request output array");
   if (cfg->policy == RS_POLICY_RL && cfg->rl_epsilon > 0.0 && !tr->policy_seed)
     return fail(RS_ERR_INVALID_ARGUMENT, "epsilon-greedy needs trace->policy_seed");
-  const WsLayout wl = ws_layout(tr->total_requests, tr->num_replays, rl_param_count(*cfg));
+  const WsLayout wl = ws_layout(tr->total_requests, tr->num_replays, rl_param_count(*cfg),
+                                run_tail_ints(*cfg, tr->num_replays));
   if (!workspace || workspace_bytes < wl.total)
     return fail(RS_ERR_INVALID_ARGUMENT, "workspace too small (rs_workspace_size)");
   cudaStream_t st = (cudaStream_t)stream;
@@ -529,9 +583,22 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
       }
       return std::min(best, 16);
     };
-    while (fast && !getenv("RS_WAIT_RING") && wcap > 8 && per_sm(L) < target) {
-      wcap >>= 1;
-      L = make_layout(*cfg, wcap, fast);
+    // Shrink the per-replay shared state until `target` replays fit per SM:
+    // first the waiting ring (longer queues continue in the global overflow
+    // list), then the running head to 32 entries (typical batches are 8-12,
+    // measured max 27: the global tail is rarely touched; the tail build of
+    // the kernel is used), then to 16.  RS_RUN_SMEM / RS_WAIT_RING pin
+    // either (tests).
+    const int rsm_env = env_int("RS_RUN_SMEM", 0);
+    const bool ring_env = getenv("RS_WAIT_RING") != nullptr;
+    int rsm = rsm_env > 0 ? rsm_env : L.rcap;
+    L = make_layout(*cfg, wcap, fast, rsm);
+    while (fast && per_sm(L) < target) {
+      if (!ring_env && wcap > 8) wcap >>= 1;
+      else if (!rsm_env && rsm > 32) rsm = 32;
+      else if (!rsm_env && rsm > 16) rsm = 16;
+      else break;
+      L = make_layout(*cfg, wcap, fast, rsm);
     }
   }
   rs::KParams kp;
@@ -637,7 +704,10 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   }
   {  // fast-kernel word offsets (fast.cuh RQ/RP/.../WE accessors)
     const int m = cfg->num_instances;
-    kp.rstride = L.rcap | 1;
+    kp.rsm = L.rsm;
+    kp.rtail = L.rcap - L.rsm;
+    kp.run_tail = kp.rtail > 0 ? reinterpret_cast<int*>(ws + wl.tail) : nullptr;
+    kp.rstride = L.rsm | 1;
     kp.f_rreq = L.off_run / 4;
     kp.f_rprompt = kp.f_rreq + m * kp.rstride;
     kp.f_rdhat = kp.f_rprompt + m * kp.rstride;
@@ -661,8 +731,6 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     kp.eps_pow2 = pow2(cfg->impact.epsilon_s, &kp.inv_eps);
     kp.kv_pow2 = pow2((double)cfg->kv_capacity_tokens, &kp.inv_kv);
     kp.mb_pow2 = pow2((double)cfg->max_batch_size, &kp.inv_mb);
-    kp.ub_max = 0;
-    for (int b = 0; b < cfg->n_predictor_edges; ++b) kp.ub_max = std::max(kp.ub_max, kp.ub[b]);
   }
 
   // warps (replays) per block: maximise resident warps per SM; the RL
@@ -706,6 +774,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   // staged once per block, which favours wider blocks).
   int sms = 0;
   RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const bool tail = fast && L.rsm < L.rcap;  // the build with the global running tail
   const int wpb_env = env_int("RS_WARPS_PER_BLOCK", 0);
   struct Plan {
     int width = 0, wpb = 0, per_sm = 0, block_smem = 0;
@@ -715,9 +784,9 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   auto plan_for = [&](int width) -> Plan {
     Plan pl;
     pl.width = width;
-    pl.kern = kernel_for(cfg->policy, fast, groups, width);
+    pl.kern = kernel_for(cfg->policy, fast, groups, width, 0, tail);
     if (!pl.kern) return pl;
-    KernelFn wide = kernel_for(cfg->policy, fast, groups, width, 1);
+    KernelFn wide = kernel_for(cfg->policy, fast, groups, width, 1, tail);
     const int gpw = rs::kWarp / width;
     // the wide RL instantiation takes blocks of up to 16 warps
     const int max_wpb = wide ? 16 : 8;
@@ -754,23 +823,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     }
     return pl;
   };
-  // Lane-group width: the whole warp.  RS_GROUP_WIDTH = 4/8/16 packs 32/W
-  // replays per warp (m <= W, whole-prompt prefill): parity-exact, but
-  // measured 7-9x SLOWER on c4 (m = 4, 16k replays): the groups of a warp
-  // diverge every tick and their paths serialise, so a warp runs its
-  // replays back to back with none of the latency hiding separate warps get.
-  // Kept as an opt-in, tested configuration, not chosen automatically.
-  const int w_env = env_int("RS_GROUP_WIDTH", 0);
-  int width = rs::kWarp;
-  if (w_env) {
-    if (w_env != 4 && w_env != 8 && w_env != 16 && w_env != 32)
-      return fail(RS_ERR_INVALID_ARGUMENT, "RS_GROUP_WIDTH must be 4, 8, 16 or 32");
-    if (fast && groups == 1) {
-      int min_w = 4;
-      while (min_w < cfg->num_instances) min_w <<= 1;
-      width = std::max(w_env, min_w);
-    }
-  }
+  const int width = rs::kWarp;  // one replay per warp
   Plan pl = plan_for(width);
   if (!pl.kern) return fail(RS_ERR_INVALID_ARGUMENT, "unknown policy");
   if (pl.wpb == 0)
@@ -787,11 +840,11 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
         if (L.weights_bytes + wpb * L.group_bytes <= smem_optin) {
           pl.wpb = wpb;
           pl.block_smem = L.weights_bytes + wpb * L.group_bytes;
-          pl.kern = kernel_for(cfg->policy, fast, groups, pl.width);  // <= 8 warps
+          pl.kern = kernel_for(cfg->policy, fast, groups, pl.width, 0, tail);  // <= 8 warps
           // one block per SM: the uncapped-register build, when it fits
           KernelFn lat = env_int("RS_NO_LAT_KERNEL", 0) ? nullptr
                                                          : kernel_for(cfg->policy, fast, groups,
-                                                                      pl.width, 2);
+                                                                      pl.width, 2, tail);
           int lat_blocks = 0;
           if (lat &&
               cudaFuncSetAttribute(lat, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -810,8 +863,8 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   // (e.g. the RL kernel with its staged Q-network): the register file is
   // not the constraint, so take the uncapped-register build there too.
   if (pl.width == rs::kWarp && pl.per_sm == 1 && pl.wpb <= 8 && pl.kern ==
-      kernel_for(cfg->policy, fast, groups, pl.width) && !env_int("RS_NO_LAT_KERNEL", 0)) {
-    KernelFn lat = kernel_for(cfg->policy, fast, groups, pl.width, 2);
+      kernel_for(cfg->policy, fast, groups, pl.width, 0, tail) && !env_int("RS_NO_LAT_KERNEL", 0)) {
+    KernelFn lat = kernel_for(cfg->policy, fast, groups, pl.width, 2, tail);
     int lat_blocks = 0;
     if (lat &&
         cudaFuncSetAttribute(lat, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.block_smem) ==
@@ -824,14 +877,14 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   }
   if (env_int("RS_DEBUG_PLAN", 0)) {
     const char* variant = !fast                                                ? "general"
-                          : pl.kern == kernel_for(cfg->policy, fast, groups, pl.width, 2) ? "lat"
-                          : pl.kern == kernel_for(cfg->policy, fast, groups, pl.width, 1) ? "wide"
+                          : pl.kern == kernel_for(cfg->policy, fast, groups, pl.width, 2, tail) ? "lat"
+                          : pl.kern == kernel_for(cfg->policy, fast, groups, pl.width, 1, tail) ? "wide"
                                                                                         : "bounded";
     fprintf(stderr,
             "rs plan: policy %d fast %d kernel %s groups %d width %d wpb %d blocks/SM %d "
-            "block_smem %d group_bytes %d weights %d wcap %d rl_global %d resident replays %lld\n",
+            "block_smem %d group_bytes %d weights %d wcap %d rsm %d rl_global %d resident replays %lld\n",
             cfg->policy, (int)fast, variant, groups, pl.width, pl.wpb, pl.per_sm, pl.block_smem,
-            L.group_bytes, L.weights_bytes, L.wcap, (int)rl_global, pl.capacity);
+            L.group_bytes, L.weights_bytes, L.wcap, L.rsm, (int)rl_global, pl.capacity);
   }
   RS_CUDA(cudaMemsetAsync(kp.work_counter, 0, sizeof(int), st));
   if (fast && !resident && env_int("RS_NO_VALIDATE_PASS", 0) == 0) {
@@ -843,7 +896,6 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     vp.arrival = kp.arrival;
     vp.prompt = kp.prompt;
     vp.decode = kp.decode;
-    vp.ub_max = kp.ub_max;
     vp.o_preempt = kp.o_preempt;
     vp.mm_removed = cfg->policy == RS_POLICY_MIN_MIN ? kp.mm_removed : nullptr;
     vp.vinfo = reinterpret_cast<int2*>(ws + wl.vinfo);

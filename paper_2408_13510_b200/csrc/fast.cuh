@@ -42,12 +42,20 @@ struct Inst {  // one instance, held in its lane's registers
   double dec_el;  // decode_batch_time for el_n running (cached)
   int el_n;
   int D, n, npf, ft;
-  int res, kv, pend, dleft, tleft, tok, nge, next_ge, next_done;
+  // kv = sum prompt-done + emitted, pend = unprefilled prompt, dleft = sum
+  // max(d_hat - emitted, 0), tleft = sum true - emitted over running.  The
+  // reservation sum and token mass follow (instance.hpp:365-368): per entry
+  // reserved = prompt + max(d_hat, emitted) = (prompt + emitted) + max(d_hat
+  // - emitted, 0), so res = kv + pend + dleft and tok = kv + pend (res_run /
+  // tok_run); neither is stored.
+  int kv, pend, dleft, tleft, nge, next_ge, next_done;
   int w_head, w_cnt, o_cnt, o_head, o_tail;
   int comps;
-  // waiting-queue aggregates in 32 bits: run_replay_fast refuses replays
-  // whose N x max(prompt + max(decode, bucket bound)) could reach 2^31
-  int resw, pendw, dlw, tlw, tokw;
+  // waiting-queue aggregates: a queue can hold every request of the replay,
+  // so these grow with the trace length (64-bit; updated only on enqueue,
+  // admission and preemption).  The running ones are bounded by the batch.
+  // (reserved over waiting = tokw + dlw, as for running)
+  long long pendw, dlw, tlw, tokw;
   // RL state encoding (encode_state, env.hpp:88-113) with the default state
   // scheme {0, e1, e2}: running entries with decode_left >= e1 / >= e2, and
   // the decode-step count D at which the next of them drops below e1 / e2
@@ -56,21 +64,107 @@ struct Inst {  // one instance, held in its lane's registers
   int ev_at;  // min(next_done, next_ge): the decode step of the next scan event
 };
 
-// running entry fields (admission order) and waiting ring fields
-__device__ __forceinline__ int& RQ(const KParams& P, int gw, int i, int j) {
-  return rs_smw[gw + P.f_rreq + i * P.rstride + j];
+// Running entry fields (admission order): request id | fresh bit, prompt,
+// d_hat, true decode, key.  Entry j < rsm of instance i in the group's
+// shared memory (odd per-instance stride: lane-owned rows hit distinct
+// banks); entries j >= rsm in the warp's global tail.  T = 0: the launch
+// has no tail (rsm = rcap) and every access is a shared-memory one; T = 1:
+// tail accesses inline (fleets whose batches often outgrow the head: c5's
+// heavy-decode m = 64); T = 2: tail accesses out of line (rare path, no
+// register cost in the tick loop).
+enum RunField { kFQ = 0, kFP = 1, kFD = 2, kFT = 3, kFK = 4 };
+
+template <int F>
+__device__ __forceinline__ int run_word(const KParams& P) {
+  return F == kFQ ? P.f_rreq : F == kFP ? P.f_rprompt : F == kFD ? P.f_rdhat
+       : F == kFT ? P.f_rtrue : P.f_rkey;
 }
-__device__ __forceinline__ int& RP(const KParams& P, int gw, int i, int j) {
-  return rs_smw[gw + P.f_rprompt + i * P.rstride + j];
+// The global tail, out of line: the rare path must not hold registers (or
+// hoisted address arithmetic) in the tick loop.
+static __device__ __noinline__ int* run_tail_ptr(const KParams& P, int f, int i, int j) {
+  const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  return P.run_tail + ((gwarp * 5 + f) * P.m + i) * P.rtail + (j - P.rsm);
 }
-__device__ __forceinline__ int& RD(const KParams& P, int gw, int i, int j) {
-  return rs_smw[gw + P.f_rdhat + i * P.rstride + j];
+template <int F>
+__device__ __forceinline__ int* run_tail_at(const KParams& P, int i, int j) {
+  return run_tail_ptr(P, F, i, j);
 }
-__device__ __forceinline__ int& RT(const KParams& P, int gw, int i, int j) {
-  return rs_smw[gw + P.f_rtrue + i * P.rstride + j];
+static __device__ __noinline__ void run_tail_put5(const KParams& P, int i, int j, int q, int pr, int dh,
+                                           int tr, int ky) {
+  int* p = run_tail_ptr(P, 0, i, j);
+  const long long fs = (long long)P.m * P.rtail;  // field stride
+  p[0] = q;
+  p[fs] = pr;
+  p[2 * fs] = dh;
+  p[3 * fs] = tr;
+  p[4 * fs] = ky;
 }
-__device__ __forceinline__ int& RK(const KParams& P, int gw, int i, int j) {
-  return rs_smw[gw + P.f_rkey + i * P.rstride + j];
+struct Ent5 {
+  int q, pr, dh, tr, ky;
+};
+static __device__ __noinline__ Ent5 run_tail_get5(const KParams& P, int i, int j) {
+  const int* p = run_tail_ptr(P, 0, i, j);
+  const long long fs = (long long)P.m * P.rtail;
+  return Ent5{p[0], p[fs], p[2 * fs], p[3 * fs], p[4 * fs]};
+}
+__device__ __forceinline__ int* run_tail_inl(const KParams& P, int f, int i, int j) {
+  const long long gwarp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  return P.run_tail + ((gwarp * 5 + f) * P.m + i) * P.rtail + (j - P.rsm);
+}
+template <int F, int T>
+__device__ __forceinline__ int rget(const KParams& P, int gw, int i, int j) {
+  if (T == 0 || j < P.rsm) return rs_smw[gw + run_word<F>(P) + i * P.rstride + j];
+  return T == 1 ? *run_tail_inl(P, F, i, j) : *run_tail_at<F>(P, i, j);
+}
+// all five fields of entry j
+template <int T>
+__device__ __forceinline__ void rput5(const KParams& P, int gw, int i, int j, int q, int pr,
+                                      int dh, int tr, int ky) {
+  if (T == 0 || j < P.rsm) {
+    const int b = gw + i * P.rstride + j;
+    rs_smw[b + P.f_rreq] = q;
+    rs_smw[b + P.f_rprompt] = pr;
+    rs_smw[b + P.f_rdhat] = dh;
+    rs_smw[b + P.f_rtrue] = tr;
+    rs_smw[b + P.f_rkey] = ky;
+  } else if (T == 1) {
+    int* p = run_tail_inl(P, 0, i, j);
+    const long long fs = (long long)P.m * P.rtail;  // field stride
+    p[0] = q;
+    p[fs] = pr;
+    p[2 * fs] = dh;
+    p[3 * fs] = tr;
+    p[4 * fs] = ky;
+  } else {
+    run_tail_put5(P, i, j, q, pr, dh, tr, ky);
+  }
+}
+template <int T>
+__device__ __forceinline__ void rget5(const KParams& P, int gw, int i, int j, int& q, int& pr,
+                                      int& dh, int& tr, int& ky) {
+  if (T == 0 || j < P.rsm) {
+    const int b = gw + i * P.rstride + j;
+    q = rs_smw[b + P.f_rreq];
+    pr = rs_smw[b + P.f_rprompt];
+    dh = rs_smw[b + P.f_rdhat];
+    tr = rs_smw[b + P.f_rtrue];
+    ky = rs_smw[b + P.f_rkey];
+  } else if (T == 1) {
+    const int* p = run_tail_inl(P, 0, i, j);
+    const long long fs = (long long)P.m * P.rtail;
+    q = p[0];
+    pr = p[fs];
+    dh = p[2 * fs];
+    tr = p[3 * fs];
+    ky = p[4 * fs];
+  } else {
+    const Ent5 e = run_tail_get5(P, i, j);
+    q = e.q;
+    pr = e.pr;
+    dh = e.dh;
+    tr = e.tr;
+    ky = e.ky;
+  }
 }
 __device__ __forceinline__ int& WQ(const KParams& P, int gw, int i, int s) {
   return rs_smw[gw + P.f_wreq + i * P.wcap + s];
@@ -93,16 +187,19 @@ __device__ __forceinline__ void inst_init(Inst& I) {
   I.dec_el = 0.0;
   I.el_n = -1;
   I.D = I.n = I.npf = I.ft = 0;
-  I.res = I.kv = I.pend = I.dleft = I.tleft = I.tok = I.nge = 0;
+  I.kv = I.pend = I.dleft = I.tleft = I.nge = 0;
   I.next_ge = I.next_done = kBig;
   I.w_head = I.w_cnt = I.o_cnt = 0;
   I.o_head = I.o_tail = (int)kNil;
   I.comps = 0;
-  I.resw = I.pendw = I.dlw = I.tlw = I.tokw = 0;
+  I.pendw = I.dlw = I.tlw = I.tokw = 0;
   I.sb1 = I.sb2 = 0;
   I.nx1 = I.nx2 = kBig;
   I.ev_at = kBig;
 }
+
+__device__ __forceinline__ int res_run(const Inst& I) { return I.kv + I.pend + I.dleft; }
+__device__ __forceinline__ int tok_run(const Inst& I) { return I.kv + I.pend; }
 
 // state-bucket tracking of one running entry with decode_left dl at step D
 __device__ __forceinline__ void sb_add(const KParams& P, Inst& I, int dl) {
@@ -118,11 +215,10 @@ __device__ __forceinline__ void sb_add(const KParams& P, Inst& I, int dl) {
 }
 
 __device__ __forceinline__ void waitagg(Inst& I, int prompt, int dhat, int tru, int emit, int s) {
-  I.resw += s * reserved_of(prompt, dhat, emit);
-  I.pendw += s * prompt;
-  I.dlw += s * (dhat > emit ? dhat - emit : 0);
-  I.tlw += s * (tru > emit ? tru - emit : 0);
-  I.tokw += s * (prompt + emit);
+  I.pendw += (long long)(s * prompt);
+  I.dlw += (long long)(s * (dhat > emit ? dhat - emit : 0));
+  I.tlw += (long long)(s * (tru > emit ? tru - emit : 0));
+  I.tokw += (long long)(s * (prompt + emit));
 }
 
 // ---- per-lane waiting queue (shared ring + global overflow list) --------
@@ -210,22 +306,16 @@ __device__ __forceinline__ void lane_push_front(const KParams& P, int gw, long l
 }
 
 // Append an admitted request to the running batch (instance.hpp:187-192).
+template <int T>
 __device__ __forceinline__ void lane_admit_one(const KParams& P, int gw, int i, Inst& I, int req,
                                                int prompt, int dhat, int tru, int emit) {
-  const int j = I.n;
-  RQ(P, gw, i, j) = req | (emit == 0 ? kFresh : 0);
-  RP(P, gw, i, j) = prompt;
-  RD(P, gw, i, j) = dhat;
-  RT(P, gw, i, j) = tru;
-  RK(P, gw, i, j) = emit - I.D;
+  rput5<T>(P, gw, i, I.n, req | (emit == 0 ? kFresh : 0), prompt, dhat, tru, emit - I.D);
   I.n++;
   I.npf++;
-  I.res += reserved_of(prompt, dhat, emit);
   I.pend += prompt;
   I.kv += emit;
   I.dleft += dhat > emit ? dhat - emit : 0;
   I.tleft += tru - emit;
-  I.tok += prompt + emit;
   const int ge_at = dhat - emit + I.D;
   if (ge_at <= I.D) I.nge++;
   else I.next_ge = ge_at < I.next_ge ? ge_at : I.next_ge;
@@ -237,16 +327,17 @@ __device__ __forceinline__ void lane_admit_one(const KParams& P, int gw, int i, 
 }
 
 // Instance::admit_waiting (instance.hpp:149-195) by the owning lane.
+template <int T>
 __device__ inline void lane_admit(const KParams& P, int gw, long long off, int i, Inst& I) {
   while (I.w_cnt > 0 && I.n < P.max_batch) {
     if (P.batching == RS_BATCHING_FCFS) {  // strict head of line
       const int s = I.w_head;
       const int prompt = WP(P, gw, i, s), dhat = WD(P, gw, i, s), emit = WE(P, gw, i, s);
-      if (I.res + reserved_of(prompt, dhat, emit) > P.kv_cap) break;
+      if (res_run(I) + reserved_of(prompt, dhat, emit) > P.kv_cap) break;
       const int req = WQ(P, gw, i, s), tru = WT(P, gw, i, s);
       I.w_head = s + 1 == P.wcap ? 0 : s + 1;
       I.w_cnt--;
-      lane_admit_one(P, gw, i, I, req, prompt, dhat, tru, emit);
+      lane_admit_one<T>(P, gw, i, I, req, prompt, dhat, tru, emit);
       lane_refill(P, gw, off, i, I);
       continue;
     }
@@ -260,7 +351,7 @@ __device__ inline void lane_admit(const KParams& P, int gw, long long off, int i
       if (s >= P.wcap) s -= P.wcap;
       const int prompt = WP(P, gw, i, s), dhat = WD(P, gw, i, s), emit = WE(P, gw, i, s);
       const int need = reserved_of(prompt, dhat, emit);
-      if (I.res + need > P.kv_cap) continue;
+      if (res_run(I) + need > P.kv_cap) continue;
       const int key = bp ? -need : (dhat > emit ? dhat - emit : 0);
       if (!found || key < bkey) { found = true; bkey = key; pos = q; }
     }
@@ -269,7 +360,7 @@ __device__ inline void lane_admit(const KParams& P, int gw, long long off, int i
       const int prompt = P.prompt[off + cur], emit = P.ov_emit[off + cur];
       const int dhat = P.ub[P.bucket[off + cur]];
       const int need = reserved_of(prompt, dhat, emit);
-      if (I.res + need <= P.kv_cap) {
+      if (res_run(I) + need <= P.kv_cap) {
         const int key = bp ? -need : (dhat > emit ? dhat - emit : 0);
         if (!found || key < bkey) { found = true; bkey = key; pos = I.w_cnt + q; preq = cur; }
       }
@@ -289,13 +380,13 @@ __device__ inline void lane_admit(const KParams& P, int gw, long long off, int i
                  WT(P, gw, i, s1), WE(P, gw, i, s1));
       }
       I.w_cnt--;
-      lane_admit_one(P, gw, i, I, req, prompt, dhat, tru, emit);
+      lane_admit_one<T>(P, gw, i, I, req, prompt, dhat, tru, emit);
       lane_refill(P, gw, off, i, I);
     } else {
       const int prompt = P.prompt[off + preq], tru = P.decode[off + preq];
       const int dhat = P.ub[P.bucket[off + preq]], emit = P.ov_emit[off + preq];
       lane_ov_unlink(P, off, I, preq);
-      lane_admit_one(P, gw, i, I, preq, prompt, dhat, tru, emit);
+      lane_admit_one<T>(P, gw, i, I, preq, prompt, dhat, tru, emit);
     }
   }
 }
@@ -307,24 +398,23 @@ __device__ inline void lane_admit(const KParams& P, int gw, long long off, int i
 // group streams the batch in W-entry chunks, compacting as it goes (an
 // entry only ever moves down, onto a slot already read).
 // SB: also recount the RL state-bucket tracking (Inst::sb1..nx2).
-template <int W, bool SB>
+template <int W, bool SB, int T>
 __device__ inline void warp_scan_instance(const KParams& P, int gw, long long off, int i,
                                           int owner, Inst& I, const Lanes<W>& L) {
   const int l = L.l;
+  if (T) L.sync();  // the owner's global-tail writes before any lane reads them
   const int D = L.shfl(I.D, owner);
   const int n = L.shfl(I.n, owner);
   const double clock = L.shfl(I.clock, owner);
-  int res = 0, kv = 0, dl = 0, tl = 0, tok = 0, nge = 0, nxg = kBig, nxd = kBig;
+  int kv = 0, dl = 0, tl = 0, nge = 0, nxg = kBig, nxd = kBig;
   int s1 = 0, s2 = 0, x1 = kBig, x2 = kBig;
   int ncomp = 0;
   auto account = [&](int pr, int dh, int tr, int ky) {
     const int em = D + ky;
-    res += reserved_of(pr, dh, em);
     kv += pr + em;
     const int d = dh - em;
     dl += d > 0 ? d : 0;
     tl += tr - em;
-    tok += pr + em;
     if (em >= dh) nge++;
     else nxg = min(nxg, dh - ky);
     nxd = min(nxd, tr - ky);
@@ -346,11 +436,7 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
       if (k * kWarp < n) {
         bool done = false;
         if (j < n) {
-          rq[k] = RQ(P, gw, i, j);
-          pr[k] = RP(P, gw, i, j);
-          dh[k] = RD(P, gw, i, j);
-          tr[k] = RT(P, gw, i, j);
-          ky[k] = RK(P, gw, i, j);
+          rget5<T>(P, gw, i, j, rq[k], pr[k], dh[k], tr[k], ky[k]);
           done = D + ky[k] >= tr[k];
           if (done) P.o_completion[off + (rq[k] & kReqMask)] = clock;
           keep[k] = !done;
@@ -366,11 +452,7 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
           const unsigned km = L.ballot(keep[k]);
           if (keep[k]) {
             const int d = npos + __popc(km & L.lt());
-            RQ(P, gw, i, d) = rq[k];
-            RP(P, gw, i, d) = pr[k];
-            RD(P, gw, i, d) = dh[k];
-            RT(P, gw, i, d) = tr[k];
-            RK(P, gw, i, d) = ky[k];
+            rput5<T>(P, gw, i, d, rq[k], pr[k], dh[k], tr[k], ky[k]);
           }
           npos += __popc(km);
         }
@@ -383,11 +465,7 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
       int rq = 0, pr = 0, dh = 0, tr = 0, ky = 0;
       bool keep = false;
       if (j < n) {
-        rq = RQ(P, gw, i, j);
-        pr = RP(P, gw, i, j);
-        dh = RD(P, gw, i, j);
-        tr = RT(P, gw, i, j);
-        ky = RK(P, gw, i, j);
+        rget5<T>(P, gw, i, j, rq, pr, dh, tr, ky);
         const bool done = D + ky >= tr;
         if (done) P.o_completion[off + (rq & kReqMask)] = clock;
         keep = !done;
@@ -400,22 +478,16 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
       if (keep) {
         const int d = c - before + __popc(km & L.lt());
         if (d != j) {
-          RQ(P, gw, i, d) = rq;
-          RP(P, gw, i, d) = pr;
-          RD(P, gw, i, d) = dh;
-          RT(P, gw, i, d) = tr;
-          RK(P, gw, i, d) = ky;
+          rput5<T>(P, gw, i, d, rq, pr, dh, tr, ky);
         }
       }
       if (keep) account(pr, dh, tr, ky);
       L.sync();
     }
   }
-  res = L.sum(res);
   kv = L.sum(kv);
   dl = L.sum(dl);
   tl = L.sum(tl);
-  tok = L.sum(tok);
   nge = L.sum(nge);
   nxg = L.min(nxg);
   nxd = L.min(nxd);
@@ -435,13 +507,11 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
     }
     I.n = n - ncomp;
     I.comps += ncomp;
-    I.res = res;
     I.kv = kv;
     I.pend = 0;
     I.npf = 0;
     I.dleft = dl;
     I.tleft = tl;
-    I.tok = tok;
     I.nge = nge;
     I.next_ge = nxg;
     I.next_done = nxd;
@@ -452,29 +522,26 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
 
 // Serial (owner lane) recount of every running aggregate after preemption.
 // No request can complete here: completions were handled this step.
+template <int T>
 __device__ inline void lane_recount(const KParams& P, int gw, int i, Inst& I) {
-  int res = 0, kv = 0, dl = 0, tl = 0, tok = 0, nge = 0, nxg = kBig, nxd = kBig;
+  int kv = 0, dl = 0, tl = 0, nge = 0, nxg = kBig, nxd = kBig;
   I.sb1 = I.sb2 = 0;
   I.nx1 = I.nx2 = kBig;
   for (int j = 0; j < I.n; ++j) {
-    const int pr = RP(P, gw, i, j), dh = RD(P, gw, i, j), tr = RT(P, gw, i, j),
-              ky = RK(P, gw, i, j);
+    const int pr = rget<kFP, T>(P, gw, i, j), dh = rget<kFD, T>(P, gw, i, j),
+              tr = rget<kFT, T>(P, gw, i, j), ky = rget<kFK, T>(P, gw, i, j);
     const int em = I.D + ky;
-    res += reserved_of(pr, dh, em);
     kv += pr + em;
     dl += dh > em ? dh - em : 0;
     tl += tr - em;
-    tok += pr + em;
     if (em >= dh) nge++;
     else nxg = min(nxg, dh - ky);
     nxd = min(nxd, tr - ky);
     sb_add(P, I, dh - em);
   }
-  I.res = res;
   I.kv = kv;
   I.dleft = dl;
   I.tleft = tl;
-  I.tok = tok;
   I.nge = nge;
   I.next_ge = nxg;
   I.next_done = nxd;
@@ -484,20 +551,22 @@ __device__ inline void lane_recount(const KParams& P, int gw, int i, Inst& I) {
 // preempt_if_needed (instance.hpp:282-299) by the owning lane.  Running is
 // in admission order, so the newest admission is last; all prompts are
 // prefilled at a step boundary.
+template <int T>
 __device__ __forceinline__ void lane_preempt(const KParams& P, int gw, long long off, int i,
                                              Inst& I) {
   while (I.kv > P.kv_cap && I.n > 1) {
     const int j = I.n - 1;
-    const int req = RQ(P, gw, i, j) & kReqMask, prompt = RP(P, gw, i, j),
-              dhat = RD(P, gw, i, j), tru = RT(P, gw, i, j);
-    const int emit = I.D + RK(P, gw, i, j);
+    int req, prompt, dhat, tru, key;
+    rget5<T>(P, gw, i, j, req, prompt, dhat, tru, key);
+    req &= kReqMask;
+    const int emit = I.D + key;
     I.kv -= prompt + emit;
     I.n--;
     P.o_preempt[off + req] += 1;
     lane_push_front(P, gw, off, i, I, req, prompt, dhat, tru, emit);
   }
   if (I.ft > I.n) I.ft = I.n;
-  lane_recount(P, gw, i, I);
+  lane_recount<T>(P, gw, i, I);
 }
 
 }  // namespace rs

@@ -9,8 +9,9 @@ namespace rs {
 // boundary, from the maintained aggregates.  At a step boundary every
 // admitted prompt has been prefilled (whole-prompt prefill), so running
 // prompt-bucket counts and pending running prompt tokens are zero.
-struct FeatI {  // 32-bit InstanceFeatures subset (fast kernel)
-  int res, pend, dleft, tleft, tok, cnt, kv, nrun, mind;
+struct FeatI {  // InstanceFeatures subset (fast kernel)
+  long long res, pend, dleft, tleft, tok;  // running + waiting (queues grow with the trace)
+  int cnt, kv, nrun, mind;
 };
 
 __device__ __forceinline__ bool can_accept(const KParams& P, const FeatI& f, int need) {
@@ -19,11 +20,11 @@ __device__ __forceinline__ bool can_accept(const KParams& P, const FeatI& f, int
 
 __device__ __forceinline__ FeatI feat_of(const Inst& I) {
   FeatI f;
-  f.res = I.res + I.resw;
+  f.res = (long long)res_run(I) + I.tokw + I.dlw;  // reserved = token mass + decode left
   f.pend = I.pend + I.pendw;
   f.dleft = I.dleft + I.dlw;
   f.tleft = I.tleft + I.tlw;
-  f.tok = I.tok + I.tokw;
+  f.tok = (long long)tok_run(I) + I.tokw;
   f.cnt = I.n + I.w_cnt + I.o_cnt;
   f.kv = I.kv;
   f.nrun = I.n;
@@ -72,7 +73,7 @@ __device__ __forceinline__ int grp_argmax_key(const Lanes<W>& L, unsigned long l
   return ok ? __ffs(ok) - 1 : -1;
 }
 
-template <int POL, int G, int W>
+template <int POL, int G, int W, int T>
 __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Replay& R,
                                   Inst (&S)[G], bool has_head, const Rec& hr, int hb,
                                   char* gbase, const Lanes<W>& L) {
@@ -155,13 +156,13 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
             I.sb1 = I.sb2 = 0;
             I.nx1 = I.nx2 = kBig;
             for (int j = 0; j < I.n; ++j)
-              sb_add(P, I, RD(P, gw, i, j) - (I.D + RK(P, gw, i, j)));
+              sb_add(P, I, rget<kFD, T>(P, gw, i, j) - (I.D + rget<kFK, T>(P, gw, i, j)));
           }
           cge[1] = I.sb1;
           cge[2] = I.sb2;
         } else {
           for (int j = 0; j < S[g].n; ++j) {
-            int d = RD(P, gw, i, j) - (S[g].D + RK(P, gw, i, j));
+            int d = rget<kFD, T>(P, gw, i, j) - (S[g].D + rget<kFK, T>(P, gw, i, j));
             d = d > 0 ? d : 0;
 #pragma unroll
             for (int b = 1; b < RS_MAX_BUCKETS; ++b)
@@ -370,20 +371,15 @@ __device__ __forceinline__ void load_window_fast(const KParams& P, Replay& R,
     const int j = R.a_base + l;
     const bool v = j < R.n;
     bool bad = false;
-    int vm = 0;
     if (v) {
       const long long g = R.off + j;
       const int p = P.prompt[g], d = P.decode[g];
       bad = p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens;
-      vm = p + (d > P.ub_max ? d : P.ub_max);
     }
     const double up = L.shfl_up(R.a_val, 1);
     const double prev = l == 0 ? prev_last : up;
     if (v && j > 0 && R.a_val < prev) bad = true;
-    vm = L.max(vm);
-    R.vmax = vm > R.vmax ? vm : R.vmax;
     if (L.any(bad)) R.status = RS_REPLAY_INVALID_TRACE;
-    else if ((long long)R.n * R.vmax > (1ll << 30)) R.status = RS_REPLAY_CAPACITY;
   } else {
     load_arrival_window(P, R, L);
   }
@@ -420,7 +416,7 @@ enum FastRun { kDone = 0, kRerunSeq = 1, kRerunInit = 2 };
 // ends unfinished (livelock, max_ticks, errors: rare) is re-run with init.
 // `seq` steps instances one at a time in index order (exact stop point of a
 // "nothing admissible" error).
-template <int POL, int G, int W, bool SEQ>
+template <int POL, int G, int W, bool SEQ, int T>
 __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const MlpView& M, int r,
                                    bool init, const Lanes<W>& L) {
   constexpr bool seq = SEQ;  // compile-time: the index-order re-run is a separate instantiation
@@ -433,11 +429,8 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
   int* front = reinterpret_cast<int*>(gbase + P.off_front);
 
   bool bad = false;
-  int vmax = 0;
   if (!init && P.vinfo) {  // validated and zeroed by the validate_kernel pre-pass
-    const int2 v = P.vinfo[r];
-    bad = v.x != 0;
-    vmax = v.y;
+    bad = P.vinfo[r].x != 0;
   } else for (int j = l; j < R.n; j += W) {
     const long long g = off + j;
     if (init) {
@@ -452,13 +445,8 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
     const int p = P.prompt[g], d = P.decode[g];
     if (p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens) bad = true;
     if (j > 0 && P.arrival[g] < P.arrival[g - 1]) bad = true;
-    const int v = p + (d > P.ub_max ? d : P.ub_max);
-    vmax = v > vmax ? v : vmax;
   }
   bad = L.any(bad);
-  // 32-bit aggregate guard: every per-instance token sum is bounded by
-  // N x max(prompt + max(decode, bucket bound)) (+ the running batch)
-  const bool too_big = (long long)R.n * L.max(vmax) > (1ll << 30);
   Inst S[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) inst_init(S[g]);
@@ -484,7 +472,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
   unsigned long long* pst = reinterpret_cast<unsigned long long*>(gbase + P.off_pred);
   R.pred_pos = 312;
   R.a_val = 0.0;
-  R.resident_seen = R.vmax = 0;
+  R.resident_seen = 0;
   if (P.predict_inline && P.predictor_mode == RS_PREDICTOR_SIMULATED)
     mt_seed(pst, P.predictor_seed[r], L);  // Rng(predictor_seed), env.hpp:173
   L.sync();
@@ -498,7 +486,6 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
   R.hr_q = -1;
   R.hr_prompt = R.hr_true = R.hr_bucket = 0;
   if (bad) R.status = RS_REPLAY_INVALID_TRACE;
-  else if (too_big) R.status = RS_REPLAY_CAPACITY;
   else if (R.status == RS_REPLAY_FINISHED) inject_fast(P, R, pst, L);
   next_arrival();
 
@@ -527,7 +514,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
     } else {
       hr.req = hr.prompt = hr.dhat = hr.tru = hr.emit = 0;
     }
-    const int action = decide_fast<POL, G, W>(P, gw, M, R, S, has_head, hr, hb, gbase, L);
+    const int action = decide_fast<POL, G, W, T>(P, gw, M, R, S, has_head, hr, hb, gbase, L);
     R.hash = hash_action(R.hash, action);
     // env.hpp:252-254: only an agent can produce an out-of-range action (the
     // heuristics return 0..m by construction)
@@ -616,7 +603,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
         bool prefill = false;
         if (I.w_cnt > 0 && I.n < P.max_batch) {
           const int w0 = I.w_cnt + I.o_cnt;
-          lane_admit(P, gw, off, i, I);
+          lane_admit<T>(P, gw, off, i, I);
           wdelta += I.w_cnt + I.o_cnt - w0;
           if (I.n == 0) {  // logic_error, instance.hpp:209-211
             ev = true;
@@ -643,12 +630,10 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
           I.D++;
           I.kv += n;
           I.tleft -= n;
-          I.tok += n;
-          I.res += I.nge;
           I.dleft -= n - I.nge;
           if (I.ft < n) {  // first tokens of requests admitted since the last decode
             for (int j = I.ft; j < n; ++j) {
-              const int q = RQ(P, gw, i, j);
+              const int q = rget<kFQ, T>(P, gw, i, j);
               if (q & kFresh) P.o_first[off + (q & kReqMask)] = I.clock;
             }
             I.ft = n;
@@ -667,8 +652,6 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
             I.D++;
             I.kv += n;
             I.tleft -= n;
-            I.tok += n;
-            I.res += I.nge;
             I.dleft -= n - I.nge;
             if (I.D >= I.ev_at || I.kv > P.kv_cap) {
               ev = true;
@@ -714,11 +697,11 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
         while (sm) {
           const int owner = __ffs(sm) - 1;
           sm &= sm - 1;
-          warp_scan_instance<W, POL == RS_POLICY_RL>(P, gw, off, g * W + owner, owner, S[g], L);
+          warp_scan_instance<W, POL == RS_POLICY_RL, T>(P, gw, off, g * W + owner, owner, S[g], L);
         }
         if (mine && S[g].kv > P.kv_cap && S[g].n > 1) {
           const int w0 = S[g].w_cnt + S[g].o_cnt;
-          lane_preempt(P, gw, off, g * W + l, S[g]);
+          lane_preempt<T>(P, gw, off, g * W + l, S[g]);
           wdelta += S[g].w_cnt + S[g].o_cnt - w0;
         }
       }
@@ -753,7 +736,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
   return kDone;
 }
 
-template <int POL, int G, int W>
+template <int POL, int G, int W, int T>
 __device__ __forceinline__ void replay_fast_body(const KParams& P) {
   extern __shared__ __align__(16) char smem[];
   const Lanes<W> L = make_lanes<W>();
@@ -783,25 +766,26 @@ __device__ __forceinline__ void replay_fast_body(const KParams& P) {
     if (L.l == 0) r = atomicAdd(P.work_counter, 1);
     r = L.shfl(r, 0);
     if (r >= P.num_replays) break;
-    const FastRun o = run_replay_fast<POL, G, W, false>(P, gw, gbase, M, r, false, L);
-    if (o == kRerunSeq) run_replay_fast<POL, G, W, true>(P, gw, gbase, M, r, true, L);
-    else if (o == kRerunInit) run_replay_fast<POL, G, W, false>(P, gw, gbase, M, r, true, L);
+    const FastRun o = run_replay_fast<POL, G, W, false, T>(P, gw, gbase, M, r, false, L);
+    if (o == kRerunSeq) run_replay_fast<POL, G, W, true, T>(P, gw, gbase, M, r, true, L);
+    else if (o == kRerunInit) run_replay_fast<POL, G, W, false, T>(P, gw, gbase, M, r, true, L);
   }
 }
 
-// Up to 8 replay warps per block.
-template <int POL, int G, int W>
-__global__ void __launch_bounds__(256) replay_fast_kernel(const __grid_constant__ KParams P) {
-  replay_fast_body<POL, G, W>(P);
+// Up to 8 replay warps per block, two blocks per SM (<= 128 registers: the
+// throughput regime wants 16 resident replays per SM).
+template <int POL, int G, int W, int T>
+__global__ void __launch_bounds__(256, 2) replay_fast_kernel(const __grid_constant__ KParams P) {
+  replay_fast_body<POL, G, W, T>(P);
 }
 
 // Latency regime (every replay resident in one wave, <= 8 warps per SM):
 // no launch bound, so ptxas keeps the whole tick loop in registers (158 for
 // workload_aware, no spills) instead of capping at 128 with ~450 B of spill
 // traffic on the tick chain; one such block per SM fits the register file.
-template <int POL, int G, int W>
+template <int POL, int G, int W, int T>
 __global__ void replay_fast_kernel_lat(const __grid_constant__ KParams P) {
-  replay_fast_body<POL, G, W>(P);
+  replay_fast_body<POL, G, W, T>(P);
 }
 
 // Up to 16 (the RL policy in the throughput regime): its Q-network is staged
@@ -809,9 +793,9 @@ __global__ void replay_fast_kernel_lat(const __grid_constant__ KParams P) {
 // replay slots (512 threads x 128 registers = the register file).  A separate
 // instantiation: the 512-thread bound changes the code ptxas generates, and
 // blocks of <= 8 warps run faster with the 256-thread build (measured, c3).
-template <int POL, int G, int W>
+template <int POL, int G, int W, int T>
 __global__ void __launch_bounds__(512) replay_fast_kernel_wide(const __grid_constant__ KParams P) {
-  replay_fast_body<POL, G, W>(P);
+  replay_fast_body<POL, G, W, T>(P);
 }
 
 }  // namespace rs

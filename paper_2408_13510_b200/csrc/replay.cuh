@@ -62,7 +62,7 @@ struct Replay {  // per-replay registers (uniform across the warp)
   double next_arr;
   int hr_q, hr_prompt, hr_true, hr_bucket;
   int pred_pos;  // fused predictor: next unread mt19937_64 output (312 = regenerate)
-  int resident_seen, vmax;  // streamed inputs: watermark seen, running token bound
+  int resident_seen;  // streamed inputs: watermark seen
 };
 
 __device__ __forceinline__ Grp make_grp(const KParams& P, char* base) {

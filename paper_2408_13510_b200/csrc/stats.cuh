@@ -257,38 +257,31 @@ struct ValidateParams {
   const double* arrival;
   const int* prompt;
   const int* decode;
-  int ub_max;
   int* o_preempt;
   uint8_t* mm_removed;  // may be null
-  int2* vinfo;          // per replay: {bad, max(prompt + max(decode, ub_max))}
+  int2* vinfo;          // per replay: {bad, 0}
 };
 
 __global__ void __launch_bounds__(kStatsThreads) validate_kernel(const __grid_constant__ ValidateParams P) {
-  __shared__ int s_bad, s_vmax;
+  __shared__ int s_bad;
   const int t = threadIdx.x;
   for (int r = blockIdx.x; r < P.num_replays; r += gridDim.x) {
     const long long off = P.offsets[r];
     const int n = (int)(P.offsets[r + 1] - off);
-    if (t == 0) {
-      s_bad = 0;
-      s_vmax = 0;
-    }
+    if (t == 0) s_bad = 0;
     __syncthreads();
-    int bad = 0, vmax = 0;
+    int bad = 0;
     for (int j = t; j < n; j += kStatsThreads) {
       const long long g = off + j;
       const int p = P.prompt[g], d = P.decode[g];
       if (p < 1 || p > (1 << 20) || d < 1 || d > (1 << 20)) bad = 1;
       if (j > 0 && P.arrival[g] < P.arrival[g - 1]) bad = 1;
-      const int v = p + (d > P.ub_max ? d : P.ub_max);
-      vmax = v > vmax ? v : vmax;
       P.o_preempt[g] = 0;
       if (P.mm_removed) P.mm_removed[g] = 0;
     }
     if (bad) atomicOr(&s_bad, 1);
-    atomicMax(&s_vmax, vmax);
     __syncthreads();
-    if (t == 0) P.vinfo[r] = make_int2(s_bad, s_vmax);
+    if (t == 0) P.vinfo[r] = make_int2(s_bad, 0);
     __syncthreads();
   }
 }

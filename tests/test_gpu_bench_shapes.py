@@ -71,7 +71,7 @@ def plan_field(plan, key):
 @pytest.fixture
 def debug_plan(monkeypatch):
     monkeypatch.setenv("RS_DEBUG_PLAN", "1")
-    for k in ("RS_FORCE_GENERAL", "RS_STREAM_INPUTS", "RS_GROUP_WIDTH", "RS_WAIT_RING",
+    for k in ("RS_FORCE_GENERAL", "RS_STREAM_INPUTS", "RS_RUN_SMEM", "RS_WAIT_RING",
               "RS_WARPS_PER_BLOCK", "RS_RL_GLOBAL"):
         monkeypatch.delenv(k, raising=False)
 
@@ -166,3 +166,15 @@ def test_c5_shape_large_fleet(gpu, debug_plan, capfd):
     arrs, stats, plan = run_batch(gpu, cfg, tb, ps, capfd)
     assert plan_field(plan, "groups") == "2", plan
     check_sample(cfg, tb, ps, arrs, stats, [0, 1, 2, 300, R - 1], [2, R - 1])
+
+
+def test_300k_request_replay(gpu, debug_plan, capfd):
+    # Beyond the round-1 32-bit aggregate guard (N x max(prompt + max(decode,
+    # 4096)) <= 2^30, i.e. about 210k requests): the waiting-queue aggregates
+    # are 64-bit, so a 300k-request replay runs, bit-exact (c2's fleet and
+    # arrival rate, ~750k ticks).
+    tb, ps = seed_batch([9, 10], 300_000, 20.0)
+    cfg = abi.default_config("workload_aware", 8)
+    arrs, stats, plan = run_batch(gpu, cfg, tb, ps, capfd)
+    assert np.all(stats["status"] == abi.REPLAY_FINISHED)
+    check_sample(cfg, tb, ps, arrs, stats, [0, 1], [])

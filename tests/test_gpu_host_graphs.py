@@ -74,7 +74,7 @@ class Call:
 
 def test_graph_replay_after_other_shape(gpu, monkeypatch):
     monkeypatch.setenv("RS_STREAM_INPUTS", "1")  # stream (watermarked) even small inputs
-    for k in ("RS_NO_GRAPH", "RS_DEBUG_TIMING", "RS_FORCE_GENERAL", "RS_GROUP_WIDTH"):
+    for k in ("RS_NO_GRAPH", "RS_DEBUG_TIMING", "RS_FORCE_GENERAL", "RS_RUN_SMEM"):
         monkeypatch.delenv(k, raising=False)
     pin = Pinned(gpu)
     try:

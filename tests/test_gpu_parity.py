@@ -18,23 +18,23 @@ pytestmark = pytest.mark.gpu
 GOLDEN = Path(__file__).resolve().parent / "golden"
 
 
-@pytest.fixture(params=["fast", "general", "streamed", "packed"], autouse=True)
+@pytest.fixture(params=["fast", "general", "streamed", "tail"], autouse=True)
 def kernel_path(request, monkeypatch):
     """Every parity test runs on both replay kernels: the lane-per-instance
     fast kernel (whole-prompt prefill) and the general warp-per-instance one;
     "streamed" forces rs_replay_batch_host's chunked input copies overlapping
     the fast kernel (taken whenever the replays have equal lengths);
-    "packed" forces the narrowest lane group the fleet allows (32/W replays
-    per warp, W = max(4, next power of two >= m))."""
+    "tail" keeps only 2 running entries per instance in shared memory, so
+    every larger running batch continues in the warp's global tail."""
     if request.param == "general":
         monkeypatch.setenv("RS_FORCE_GENERAL", "1")
     else:
         monkeypatch.delenv("RS_FORCE_GENERAL", raising=False)
     monkeypatch.setenv("RS_STREAM_INPUTS", "1" if request.param == "streamed" else "0")
-    if request.param == "packed":
-        monkeypatch.setenv("RS_GROUP_WIDTH", "4")
+    if request.param == "tail":
+        monkeypatch.setenv("RS_RUN_SMEM", "2")
     else:
-        monkeypatch.delenv("RS_GROUP_WIDTH", raising=False)
+        monkeypatch.delenv("RS_RUN_SMEM", raising=False)
     return request.param
 
 
