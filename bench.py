@@ -572,7 +572,10 @@ def main():
                "path": "rs_replay_batch_host (C ABI, pinned host buffers, wall clock)",
                "with_per_request_d2h": {"value": ticks_total * args.steps / t_full,
                                         "d2h_bytes_per_step": int(d2h_full),
-                                        "ms_per_step": t_full * 1e3 / args.steps}}
+                                        "ms_per_step": t_full * 1e3 / args.steps,
+                                        "outputs": "every per-request array, copied back in 8 "
+                                                   "request-index chunks as the replays "
+                                                   "finalise them (streamed outputs)"}}
         for hs, st in zip(h_st, cell_stats):
             h_stats = np.frombuffer(hs.numpy().tobytes(), dtype=abi.STATS_DTYPE)
             if not np.array_equal(h_stats["decision_hash"], st["decision_hash"]):

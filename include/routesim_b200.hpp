@@ -187,6 +187,21 @@ class BatchSim {
                RewardConfig{}, 0);
   }
 
+  // run_policy with the replays sharded over several devices of this process
+  // (rs_replay_batch_multi: one shard per device, NCCL all-gather of the
+  // per-replay statistics); results identical to run_policy.
+  std::vector<ReplayResult> run_policy_multi(const std::string& policy,
+                                             const std::vector<int32_t>& devices,
+                                             long long max_ticks = 10'000'000,
+                                             const std::vector<int>& rl_dims = {},
+                                             const std::vector<double>& rl_params = {},
+                                             double epsilon = 0.0,
+                                             const std::vector<uint64_t>& policy_seeds = {}) const {
+    if (devices.empty()) throw std::invalid_argument("run_policy_multi: no devices");
+    return run(policy, max_ticks, rl_dims, rl_params, epsilon, policy_seeds, nullptr, 0,
+               RewardConfig{}, 0, &devices);
+  }
+
   // run_policy with record_trajectory: every replay's ClusterSim::trajectory()
   // (the first `capacity` ticks) into `trajectories`.
   std::vector<ReplayResult> run_trajectory(const std::string& policy, long long capacity,
@@ -208,7 +223,8 @@ class BatchSim {
                                 const std::vector<uint64_t>& policy_seeds,
                                 std::vector<std::vector<TickRecord>>* trajectories,
                                 long long capacity, const RewardConfig& reward,
-                                int episode_k) const {
+                                int episode_k,
+                                const std::vector<int32_t>* devices = nullptr) const {
     rs_batch_cfg a = to_abi(cfg_, make_policy(policy));
     a.max_ticks = max_ticks;
     if (a.policy == RS_POLICY_RL) {
@@ -252,7 +268,10 @@ class BatchSim {
     std::vector<uint8_t> pb(static_cast<size_t>(N));
     std::vector<rs_replay_stats> st(R);
     rs_req_out out{inst.data(), ro.data(), fi.data(), co.data(), pre.data(), pb.data()};
-    if (!trajectories) {
+    if (devices) {
+      check(rs_replay_batch_multi(&a, &tr, &out, st.data(), devices->data(),
+                                  static_cast<int32_t>(devices->size())));
+    } else if (!trajectories) {
       check(rs_replay_batch_host(&a, &tr, &out, st.data(), device_));
     } else {
       if (capacity < 0) throw std::invalid_argument("trajectory capacity < 0");

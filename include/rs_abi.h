@@ -154,6 +154,9 @@ typedef struct rs_batch_cfg {
    * Device pointer for rs_replay_batch, host pointer for the _host variant. */
   int32_t rl_num_layers;        /* number of affine layers (dims - 1) */
   int32_t rl_dims[RS_MAX_LAYERS + 1];
+  /* Every weight finite: the device forward skips exact-zero inputs, which
+   * equals the reference's w * 0 only for finite w (the _host entry points
+   * reject non-finite weights with RS_ERR_UNSUPPORTED). */
   const double* rl_params;
   double rl_epsilon;            /* 0 => DqnAgent::greedy; >0 => DqnAgent::act */
 

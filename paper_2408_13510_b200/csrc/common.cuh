@@ -134,6 +134,12 @@ struct KParams {
   // replay are on the device; the copy stream raises it chunk by chunk while
   // the replay runs (nullptr = everything resident, validated up front)
   const int* resident;
+  // streamed outputs (host entry point): per chunk of request indices, the
+  // count of replays whose requests below out_bounds[c] are all final
+  // (completed); nullptr = off (internal.h rs_internal_stream_out)
+  int* out_marks;
+  int n_out_bounds;
+  int out_bounds[16];
   // ClusterConfig::record_trajectory (general kernel only): per-tick reward
   // (env.hpp:257-303) and TickRecords (env.hpp:305-319)
   const int2* vinfo;    // fast kernel: per-replay {bad, 0} from validate_kernel (null: walk the trace)

@@ -532,7 +532,8 @@ bool rs_internal_fast_path(const rs_batch_cfg* cfg) {
 rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr,
                                    rs_req_out* out, rs_replay_stats* stats, void* workspace,
                                    size_t workspace_bytes, void* stream, const int* resident,
-                                   void* inputs_done, const rs_trajectory* traj) {
+                                   void* inputs_done, const rs_trajectory* traj,
+                                   const rs_internal_stream_out* sout) {
   rs_status s = validate(cfg);
   if (s != RS_OK) return s;
   if ((s = require_device()) != RS_OK) return s;
@@ -560,8 +561,10 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   // whole-prompt prefill (no chunking, m <= 64) takes the lane-per-instance
   // kernel; chunked prefill and larger fleets take the general kernel
   const bool fast = rs_internal_fast_path(cfg) && !traj;
-  if (resident && !fast)
-    return fail(RS_ERR_INVALID_ARGUMENT, "streamed inputs need the lane-per-instance kernel");
+  if ((resident || sout) && !fast)
+    return fail(RS_ERR_INVALID_ARGUMENT, "streamed inputs / outputs need the lane-per-instance kernel");
+  if (sout && (sout->nbounds < 1 || sout->nbounds > 16 || !sout->marks))
+    return fail(RS_ERR_INVALID_ARGUMENT, "streamed outputs: 1..16 chunks");
   const int groups = m_inst <= 32 ? 1 : 2;
   Layout L = make_layout(*cfg, wcap, fast);
   {
@@ -678,6 +681,11 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   kp.predictor_seed = tr->predictor_seed;
   kp.given_bucket = tr->given_bucket;
   kp.resident = resident;
+  if (sout) {
+    kp.out_marks = sout->marks;
+    kp.n_out_bounds = sout->nbounds;
+    for (int c = 0; c < sout->nbounds; ++c) kp.out_bounds[c] = sout->bounds[c];
+  }
   if (traj) {  // ClusterConfig::record_trajectory (general kernel)
     kp.traj = *traj;
     kp.traj_on = 1;
@@ -898,6 +906,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     vp.decode = kp.decode;
     vp.o_preempt = kp.o_preempt;
     vp.mm_removed = cfg->policy == RS_POLICY_MIN_MIN ? kp.mm_removed : nullptr;
+    vp.o_completion = sout ? kp.o_completion : nullptr;  // "not completed" for publish_final
     vp.vinfo = reinterpret_cast<int2*>(ws + wl.vinfo);
     const int vgrid = std::max(1, std::min(tr->num_replays, sms * 8));
     rs::validate_kernel<<<vgrid, rs::kStatsThreads, 0, st>>>(vp);
@@ -911,6 +920,16 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   // the streamed-input caller launches them itself once its copies are queued
   if (inputs_done == kDeferStats) return RS_OK;
   return rs_internal_stats(tr, out, stats, stream, inputs_done);
+}
+
+rs_status rs_internal_check_weights(const double* params, size_t count) {
+  if (!params) return fail(RS_ERR_INVALID_ARGUMENT, "rl: null parameters");
+  for (size_t k = 0; k < count; ++k)
+    if (!std::isfinite(params[k]))
+      return fail(RS_ERR_UNSUPPORTED,
+                  "rl: non-finite Q-network weight " + std::to_string(k) +
+                      " (the forward skips exact-zero inputs, exact only for finite weights)");
+  return RS_OK;
 }
 
 rs_status rs_internal_stats(const rs_trace_soa* tr, const rs_req_out* out, rs_replay_stats* stats,

@@ -416,9 +416,32 @@ enum FastRun { kDone = 0, kRerunSeq = 1, kRerunInit = 2 };
 // ends unfinished (livelock, max_ticks, errors: rare) is re-run with init.
 // `seq` steps instances one at a time in index order (exact stop point of a
 // "nothing admissible" error).
+// Streamed outputs: advance the replay's final prefix `fin` (every request
+// below it has completed: its outputs are final) and count the replay into
+// every chunk mark it has passed.  Called after ticks that completed
+// something and finished without error: a tick cut short by "nothing
+// admissible" is re-run in index order and may end with fewer completions,
+// so it publishes nothing.  The writes of the whole warp are fenced system
+// wide before a mark moves (the copy engine reads them next).
+template <int W>
+__device__ __forceinline__ void publish_final(const KParams& P, long long off, int n, int upto,
+                                           int& fin, int& fch, const Lanes<W>& L) {
+  if (L.l == 0)
+    while (fin < upto && P.o_completion[off + fin] >= 0.0) ++fin;
+  fin = L.shfl(fin, 0);
+  if (fch < P.n_out_bounds && fin >= min(P.out_bounds[fch], n)) {
+    __threadfence_system();
+    L.sync();
+    if (L.l == 0)
+      while (fch < P.n_out_bounds && fin >= min(P.out_bounds[fch], n))
+        atomicAdd(P.out_marks + fch++, 1);
+    fch = L.shfl(fch, 0);
+  }
+}
+
 template <int POL, int G, int W, bool SEQ, int T>
 __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const MlpView& M, int r,
-                                   bool init, const Lanes<W>& L) {
+                                   bool init, int& fin, int& fch, const Lanes<W>& L) {
   constexpr bool seq = SEQ;  // compile-time: the index-order re-run is a separate instantiation
   const int l = L.l;
   Replay R;
@@ -433,7 +456,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
     bad = P.vinfo[r].x != 0;
   } else for (int j = l; j < R.n; j += W) {
     const long long g = off + j;
-    if (init) {
+    if (init && j >= fin) {  // (streamed outputs: below fin already published, rewritten identically)
       P.o_instance[g] = -1;
       P.o_routed[g] = -1.0;
       P.o_first[g] = -1.0;
@@ -441,6 +464,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
     }
     P.o_preempt[g] = 0;
     if (POL == RS_POLICY_MIN_MIN) P.mm_removed[g] = 0;
+    if (P.out_marks && !init) P.o_completion[g] = -1.0;  // not completed (publish_final)
     if (P.resident) continue;  // streamed inputs: validated per window on load
     const int p = P.prompt[g], d = P.decode[g];
     if (p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens) bad = true;
@@ -712,14 +736,17 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
     for (int g = 0; g < G; ++g) {
       comps += S[g].comps;
       S[g].comps = 0;
-      // instances emptied by this tick's last events skip ahead (instance.hpp:309)
-      if (S[g].clock < t1 && S[g].n == 0 && S[g].w_cnt == 0) S[g].clock = t1;
+      // An instance emptied by this tick's last events skips ahead to t1
+      // (instance.hpp:309) lazily: nothing reads an idle instance's clock
+      // before either the next run_until (which snaps it to that tick's t1)
+      // or an enqueue (which raises it to the router clock, this t1).
     }
     // completions and waiting-count changes of the tick (two exact sums: a
     // large delta_t can admit or preempt any number of requests in one tick)
     if (L.any((comps | wdelta) != 0)) {
       R.completed += L.sum(comps);
       R.total_wait += L.sum(wdelta);
+      if (P.out_marks && L.any(comps != 0)) publish_final(P, off, R.n, R.cursor, fin, fch, L);
     }
     R.clock = t1;
     if (R.clock >= R.next_arr) {  // inject_arrivals (env.hpp:357-375) only when due
@@ -733,6 +760,16 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
   if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
   if (!init && R.status != RS_REPLAY_FINISHED) return kRerunInit;
   write_replay_stats(P, R, r, L);
+  if (P.out_marks) {  // the replay is over: every output is final
+    fin = R.n;
+    if (fch < P.n_out_bounds) {
+      __threadfence_system();
+      L.sync();
+      if (L.l == 0)
+        while (fch < P.n_out_bounds) atomicAdd(P.out_marks + fch++, 1);
+      fch = L.shfl(fch, 0);
+    }
+  }
   return kDone;
 }
 
@@ -766,9 +803,12 @@ __device__ __forceinline__ void replay_fast_body(const KParams& P) {
     if (L.l == 0) r = atomicAdd(P.work_counter, 1);
     r = L.shfl(r, 0);
     if (r >= P.num_replays) break;
-    const FastRun o = run_replay_fast<POL, G, W, false, T>(P, gw, gbase, M, r, false, L);
-    if (o == kRerunSeq) run_replay_fast<POL, G, W, true, T>(P, gw, gbase, M, r, true, L);
-    else if (o == kRerunInit) run_replay_fast<POL, G, W, false, T>(P, gw, gbase, M, r, true, L);
+    int fin = 0, fch = 0;  // streamed outputs: final prefix, next chunk mark
+    const FastRun o = run_replay_fast<POL, G, W, false, T>(P, gw, gbase, M, r, false, fin, fch, L);
+    if (o == kRerunSeq)
+      run_replay_fast<POL, G, W, true, T>(P, gw, gbase, M, r, true, fin, fch, L);
+    else if (o == kRerunInit)
+      run_replay_fast<POL, G, W, false, T>(P, gw, gbase, M, r, true, fin, fch, L);
   }
 }
 

@@ -1,6 +1,7 @@
 // host_api.cu — host-buffer entry points of the C ABI: rs_replay_batch_host
 // (the reference-facing call: H2D, predictor kernel, replay kernel, D2H) and
 // the standalone Q-network forward used for per-stage parity.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -39,6 +40,24 @@ rs_status fail2(rs_status s, const std::string& m) {
 
 size_t al(size_t v) { return (v + 255) / 256 * 256; }
 
+// cuStreamWaitValue32 (a stream waits until a device word reaches a value),
+// through the runtime's driver entry point: no link-time libcuda dependency.
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValueFn wait_value_fn() {
+  static WaitValueFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      cudaGetLastError();
+      p = nullptr;
+    }
+    return reinterpret_cast<WaitValueFn>(p);
+  }();
+  return fn;
+}
+
 // A captured rs_replay_batch_host call.  The graph's watermark copies read
 // `marks` when the graph runs, so every graph owns its pinned values, written
 // once at capture and never again (a later call of another shape cannot
@@ -58,7 +77,8 @@ struct DeviceCache {
   size_t bytes = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;      // streamed inputs (rs_replay_batch_host)
-  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+  cudaStream_t out_stream = nullptr;       // streamed outputs
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr, ev_out = nullptr;
   int* marks = nullptr;                    // pinned watermarks of direct (uncaptured) calls
   int nmarks = 0;
   std::vector<GraphEntry> graphs;          // LRU, <= kMaxGraphs
@@ -176,6 +196,8 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
   if (rl) {
     for (int l = 0; l < cfg->rl_num_layers; ++l)
       rl_bytes += ((size_t)cfg->rl_dims[l] * cfg->rl_dims[l + 1] + cfg->rl_dims[l + 1]) * sizeof(double);
+    if ((s = rs_internal_check_weights(cfg->rl_params, rl_bytes / sizeof(double))) != RS_OK)
+      return s;
   }
   size_t ws_bytes = 0;
   if ((s = forward(rs_workspace_size(cfg, R, N, &ws_bytes))) != RS_OK) return s;
@@ -199,6 +221,7 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
   const size_t o_st = o; o += al(sizeof(rs_replay_stats) * R);
   const size_t o_ws = o; o += al(ws_bytes);
   const size_t o_fl = o; o += al(4);
+  const size_t o_mk = o; o += al(4 * 16);  // streamed-output chunk marks
   // trajectory arrays (record_trajectory): one region per requested field
   const int64_t nrec = htraj ? (int64_t)R * htraj->capacity : 0;
   const int m = cfg->num_instances;
@@ -248,6 +271,38 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
   const int64_t min_stream = se ? atoll(se) : (int64_t)1 << 22;
   const bool stream_in = uniform && n_eq > 0 && min_stream > 0 && N >= min_stream &&
                          rs_internal_fast_path(cfg) && !htraj;
+  // Streamed outputs (with streamed inputs): every per-request result array
+  // goes back in chunks of request indices while the replays still run —
+  // a chunk once every replay's requests below its end have completed
+  // (their outputs final; the kernel counts replays per chunk and the out
+  // stream waits on the count), so only the last chunk's copy follows the
+  // kernel.  RS_STREAM_OUTPUTS=0 turns it off (A/B).
+  // Page-locked destinations only: a copy into pageable memory is staged
+  // through the host and would block the enqueue until the chunk is final.
+  const char* so_env = getenv("RS_STREAM_OUTPUTS");
+  auto page_locked = [](const void* q) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, q) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+  };
+  const bool stream_out = stream_in && out && out->instance && out->routed_s &&
+                          out->first_token_s && out->completion_s && out->preemptions &&
+                          out->predicted_bucket && wait_value_fn() &&
+                          !(so_env && so_env[0] == '0') && page_locked(out->instance) &&
+                          page_locked(out->routed_s) && page_locked(out->first_token_s) &&
+                          page_locked(out->completion_s) && page_locked(out->preemptions) &&
+                          page_locked(out->predicted_bucket);
+  rs_internal_stream_out sout{};
+  if (stream_out) {  // eight equal chunks of request indices
+    sout.marks = reinterpret_cast<int*>(b + o_mk);
+    for (int c = 1; c <= 8; ++c) {
+      const int e = (int)(n_eq * c / 8);
+      if (e > (sout.nbounds ? sout.bounds[sout.nbounds - 1] : 0)) sout.bounds[sout.nbounds++] = e;
+    }
+  }
   // Everything the call puts on the device, as one enqueue.  With pinned
   // host buffers and a repeated call shape it is captured once into a CUDA
   // graph and replayed with a single launch: the host does ~10 us of API
@@ -324,6 +379,7 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
       if (!dc.ev_done) RS_CUDA2(cudaEventCreateWithFlags(&dc.ev_done, cudaEventDisableTiming));
       int* flag = reinterpret_cast<int*>(b + o_fl);
       RS_CUDA2(cudaMemsetAsync(flag, 0, sizeof(int), st));
+      if (stream_out) RS_CUDA2(cudaMemsetAsync(sout.marks, 0, sizeof(int) * 16, st));
       RS_CUDA2(cudaEventRecord(dc.ev_ready, st));
       const cudaStream_t cs = dc.copy_stream;
       RS_CUDA2(cudaStreamWaitEvent(cs, dc.ev_ready, 0));
@@ -332,7 +388,7 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
       // the chunk copies (and any host hiccup meanwhile) overlaps the replay
       // instead of delaying its launch.  The stats pass waits for the copies.
       s = forward(rs_internal_replay_batch(&dcfg, &dt, &dout, dstats, b + o_ws, ws_bytes, st, flag,
-                                           kDeferStats, nullptr));
+                                           kDeferStats, nullptr, stream_out ? &sout : nullptr));
       if (s != RS_OK) return s;
       struct Col { size_t off; const void* src; size_t es; };
       const Col cols[4] = {{o_arr, tr->arrival_s, 8}, {o_pr, tr->prompt_tokens, 4},
@@ -351,6 +407,35 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
         RS_CUDA2(cudaMemcpyAsync(flag, marks + i, sizeof(int), cudaMemcpyHostToDevice, cs));
         lo = hi;
       }
+      if (stream_out) {
+        // out stream: per chunk, wait until every replay has published it,
+        // then copy its columns of every per-request array back
+        if (!dc.out_stream)
+          RS_CUDA2(cudaStreamCreateWithFlags(&dc.out_stream, cudaStreamNonBlocking));
+        if (!dc.ev_out) RS_CUDA2(cudaEventCreateWithFlags(&dc.ev_out, cudaEventDisableTiming));
+        const cudaStream_t os = dc.out_stream;
+        RS_CUDA2(cudaStreamWaitEvent(os, dc.ev_ready, 0));
+        struct OCol { void* dst; size_t off, es; };
+        const OCol ocols[6] = {{out->instance, o_in, 4},    {out->routed_s, o_ro, 8},
+                               {out->first_token_s, o_fi, 8}, {out->completion_s, o_co, 8},
+                               {out->preemptions, o_pe, 4},   {out->predicted_bucket, o_pb, 1}};
+        int lo2 = 0;
+        for (int c = 0; c < sout.nbounds; ++c) {
+          const int hi2 = sout.bounds[c];
+          if (wait_value_fn()(os, reinterpret_cast<CUdeviceptr>(sout.marks + c), (cuuint32_t)R,
+                              CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+            return fail2(RS_ERR_CUDA, "cuStreamWaitValue32 failed");
+          for (const OCol& oc : ocols) {
+            const size_t pitch = (size_t)n_eq * oc.es;
+            RS_CUDA2(cudaMemcpy2DAsync(static_cast<char*>(oc.dst) + (size_t)lo2 * oc.es, pitch,
+                                       b + oc.off + (size_t)lo2 * oc.es, pitch,
+                                       (size_t)(hi2 - lo2) * oc.es, (size_t)R,
+                                       cudaMemcpyDeviceToHost, os));
+          }
+          lo2 = hi2;
+        }
+        RS_CUDA2(cudaEventRecord(dc.ev_out, os));
+      }
       RS_CUDA2(cudaEventRecord(dc.ev_done, cs));
       s = forward(rs_internal_stats(&dt, &dout, dstats, st, dc.ev_done));
       if (s != RS_OK) {
@@ -364,7 +449,9 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
       if (!dst || n == 0) return cudaSuccess;
       return cudaMemcpyAsync(dst, b + off, n, cudaMemcpyDeviceToHost, st);
     };
-    if (out) {
+    if (stream_out) {
+      RS_CUDA2(cudaStreamWaitEvent(st, dc.ev_out, 0));  // the out stream's copies
+    } else if (out) {
       RS_CUDA2(d2h(out->instance, o_in, 4ull * N));
       RS_CUDA2(d2h(out->routed_s, o_ro, 8ull * N));
       RS_CUDA2(d2h(out->first_token_s, o_fi, 8ull * N));
@@ -411,6 +498,7 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
       put(&o, sizeof(o));
       put(&n_eq, sizeof(n_eq));
       put(&stream_in, sizeof(stream_in));
+      put(&stream_out, sizeof(stream_out));
       GraphEntry* hit = nullptr;
       for (GraphEntry& g : dc.graphs)
         if (g.key == key) hit = &g;

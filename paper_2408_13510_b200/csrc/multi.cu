@@ -276,6 +276,12 @@ extern "C" rs_status rs_replay_batch_multi(const rs_batch_cfg* cfg, const rs_tra
   for (int r = 0; r < R; ++r)
     if (tr->offsets[r + 1] < tr->offsets[r])
       return failm(RS_ERR_INVALID_ARGUMENT, "offsets must be non-decreasing");
+  if (cfg->policy == RS_POLICY_RL) {
+    size_t np = 0;
+    for (int l = 0; l < cfg->rl_num_layers; ++l)
+      np += (size_t)cfg->rl_dims[l] * cfg->rl_dims[l + 1] + cfg->rl_dims[l + 1];
+    if ((s = rs_internal_check_weights(cfg->rl_params, np)) != RS_OK) return s;
+  }
   Nccl& nc = nccl();
   if (!nc.ok) return failm(RS_ERR_UNSUPPORTED, "NCCL unavailable: " + nc.why);
 

@@ -259,6 +259,7 @@ struct ValidateParams {
   const int* decode;
   int* o_preempt;
   uint8_t* mm_removed;  // may be null
+  double* o_completion; // may be null: set to -1 (not completed; streamed outputs)
   int2* vinfo;          // per replay: {bad, 0}
 };
 
@@ -278,6 +279,7 @@ __global__ void __launch_bounds__(kStatsThreads) validate_kernel(const __grid_co
       if (j > 0 && P.arrival[g] < P.arrival[g - 1]) bad = 1;
       P.o_preempt[g] = 0;
       if (P.mm_removed) P.mm_removed[g] = 0;
+      if (P.o_completion) P.o_completion[g] = -1.0;
     }
     if (bad) atomicOr(&s_bad, 1);
     __syncthreads();

@@ -5,6 +5,7 @@
 // the golden run) and writes the reference-format report there, then runs
 // one DqnTrainer update.
 #include <cstdio>
+#include <cstring>
 
 #include "routesim_b200.hpp"
 
@@ -22,6 +23,14 @@ int main(int argc, char** argv) {
   BatchSim sim(cfg, traces, {mix_seed(777, 0x9Ded)});
   auto res = sim.run_policy("jsq");
   const rs_replay_stats& s = res[0].stats;
+  // the same batch sharded over this process's devices (device 0 here):
+  // rs_replay_batch_multi, identical results
+  auto resm = sim.run_policy_multi("jsq", {0});
+  if (std::memcmp(&resm[0].stats, &s, sizeof(rs_replay_stats)) != 0 ||
+      resm[0].completion_time_s != res[0].completion_time_s) {
+    std::printf("{\"error\": \"run_policy_multi differs from run_policy\"}\n");
+    return 4;
+  }
   if (argc > 1) {
     std::vector<std::vector<TickRecord>> traj;
     RewardConfig rw;

@@ -104,3 +104,20 @@ def test_bench_two_ranks_equal_one_rank(gpu, tmp_path):
     assert len(one) == len(two) == 64
     assert one.tobytes() == two.tobytes()
     assert '"n_gpus": 2' in line
+
+
+def test_host_entry_points_reject_non_finite_weights(gpu):
+    # the device forward skips exact-zero inputs, which equals the
+    # reference's w * 0 only for finite weights
+    tb, ps = _batch([1, 2], 200)
+    cfg = abi.default_config("rl", 4)
+    dims = [abi.state_dimension(4), 64, 64, 5]
+    params = engine.mlp_random_init(dims, 42)
+    params[17] = np.inf
+    keep = abi.set_rl(cfg, dims, params)
+    for fn, extra in ((gpu.rs_replay_batch_host, (0,)),
+                      (gpu.rs_replay_batch_multi, ((C.c_int32 * 1)(0), 1))):
+        with pytest.raises(abi.EngineError) as e:
+            _call(gpu, fn, cfg, tb, ps, *extra)
+        assert e.value.status == abi.RS_ERR_UNSUPPORTED
+    del keep

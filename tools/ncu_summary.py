@@ -72,6 +72,15 @@ def main():
     v = num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")
     if v is not None:
         pipes["shared_wavefronts"] = round(v, 2)
+    # tensor pipes (north_star asks for the MLP's tensor-pipe utilisation):
+    # every tensor-pipe percentage the report carries, the largest kept
+    tens = [num(k) for k in hdr if "tensor" in k and k.endswith("pct_of_peak_sustained_active")]
+    tens = [v for v in tens if v is not None]
+    pipes["tensor"] = round(max(tens), 3) if tens else 0.0
+    s["tensor_pipe_note"] = (
+        "the Q-network forward runs on the FP64 pipe as separately rounded DMUL + DADD "
+        "chains in the reference's summation order: tcgen05 / DMMA accumulation rounds "
+        "differently, so bit-exact parity leaves the tensor pipes idle by design")
     s["pipe_utilisation_pct"] = pipes
     for k in hdr:
         if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
