@@ -595,7 +595,9 @@ def main():
     alg_bytes = (REPLAY_BYTES_PER_REQUEST * N + REPLAY_BYTES_PER_REPLAY * R) * len(cells)
     achieved = alg_bytes / replay_s / 1e9
     traffic = None
-    prof = ROOT / "profiles" / f"ncu_replay_{args.config}.json"
+    prof = ROOT / "profiles" / "r2" / f"ncu_replay_{args.config}.json"
+    if not prof.exists():
+        prof = ROOT / "profiles" / f"ncu_replay_{args.config}.json"
     if prof.exists():
         try:
             pj = json.loads(prof.read_text())
