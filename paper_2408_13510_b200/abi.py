@@ -362,8 +362,9 @@ def _declare(lib: C.CDLL) -> None:
                                     C.c_void_p, C.c_size_t, C.c_void_p]
     lib.rs_replay_batch_host.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,
                                          C.c_int32]
-    lib.rs_replay_batch_multi.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,
-                                          C.c_void_p, C.c_int32]
+    if hasattr(lib, "rs_replay_batch_multi"):  # (older builds loaded for A/B timing lack it)
+        lib.rs_replay_batch_multi.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,
+                                              C.c_void_p, C.c_int32]
     lib.rs_replay_trajectory.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,
                                          P(Trajectory), C.c_void_p, C.c_size_t, C.c_void_p]
     lib.rs_replay_trajectory_host.argtypes = [P(BatchCfg), P(TraceSoA), P(ReqOut), C.c_void_p,

@@ -89,7 +89,9 @@ int run_cap(const rs_batch_cfg& c) {
 // with an odd per-instance stride so lane-owned rows hit distinct banks;
 // the first rsm entries of each instance in shared memory, the rest in the
 // warp's global tail).
-Layout make_layout(const rs_batch_cfg& c, int wcap, bool fast, int rsm = 0) {
+// fused = the simulated predictor draws inside the replay kernel (its
+// mt19937_64 block lives in the replay's shared slot).
+Layout make_layout(const rs_batch_cfg& c, int wcap, bool fast, int rsm = 0, bool fused = true) {
   Layout L{};
   const int m = c.num_instances;
   L.rcap = run_cap(c);
@@ -121,7 +123,8 @@ Layout make_layout(const rs_batch_cfg& c, int wcap, bool fast, int rsm = 0) {
   L.off_front = (int)off;
   if (c.policy == RS_POLICY_MIN_MIN) off = align_up(off + rs::kMaxFront * sizeof(int), 16);
   L.off_pred = (int)off;  // fused predictor's mt19937_64 state + outputs
-  if (fast && (c.flags & RS_FLAG_PREDICT_INLINE) && c.predictor_mode == RS_PREDICTOR_SIMULATED)
+  if (fast && fused && (c.flags & RS_FLAG_PREDICT_INLINE) &&
+      c.predictor_mode == RS_PREDICTOR_SIMULATED)
     off = align_up(off + 312 * sizeof(unsigned long long), 16);
   L.group_bytes = (int)align_up(off, 128);
   L.weights_bytes = 0;
@@ -533,7 +536,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
                                    rs_req_out* out, rs_replay_stats* stats, void* workspace,
                                    size_t workspace_bytes, void* stream, const int* resident,
                                    void* inputs_done, const rs_trajectory* traj,
-                                   const rs_internal_stream_out* sout) {
+                                   rs_internal_stream_out* sout) {
   rs_status s = validate(cfg);
   if (s != RS_OK) return s;
   if ((s = require_device()) != RS_OK) return s;
@@ -566,6 +569,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   if (sout && (sout->nbounds < 1 || sout->nbounds > 16 || !sout->marks))
     return fail(RS_ERR_INVALID_ARGUMENT, "streamed outputs: 1..16 chunks");
   const int groups = m_inst <= 32 ? 1 : 2;
+  bool fused = true;  // the simulated predictor inside the replay kernel
   Layout L = make_layout(*cfg, wcap, fast);
   {
     // Throughput regime (more replays than ~16 per SM, the register limit):
@@ -590,18 +594,23 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     // first the waiting ring (longer queues continue in the global overflow
     // list), then the running head to 32 entries (typical batches are 8-12,
     // measured max 27: the global tail is rarely touched; the tail build of
-    // the kernel is used), then to 16.  RS_RUN_SMEM / RS_WAIT_RING pin
-    // either (tests).
+    // the kernel is used), then the fused predictor's 2.5 KB mt19937_64
+    // block (the predictions are drawn by the predict_kernel pre-pass
+    // instead; resident inputs only), then the head to 16.  RS_RUN_SMEM /
+    // RS_WAIT_RING pin either (tests).
     const int rsm_env = env_int("RS_RUN_SMEM", 0);
     const bool ring_env = getenv("RS_WAIT_RING") != nullptr;
+    const bool can_unfuse = !resident && (cfg->flags & RS_FLAG_PREDICT_INLINE) &&
+                            cfg->predictor_mode == RS_PREDICTOR_SIMULATED;
     int rsm = rsm_env > 0 ? rsm_env : L.rcap;
-    L = make_layout(*cfg, wcap, fast, rsm);
+    L = make_layout(*cfg, wcap, fast, rsm, fused);
     while (fast && per_sm(L) < target) {
       if (!ring_env && wcap > 8) wcap >>= 1;
       else if (!rsm_env && rsm > 32) rsm = 32;
+      else if (can_unfuse && fused) fused = false;
       else if (!rsm_env && rsm > 16) rsm = 16;
       else break;
-      L = make_layout(*cfg, wcap, fast, rsm);
+      L = make_layout(*cfg, wcap, fast, rsm, fused);
     }
   }
   rs::KParams kp;
@@ -681,11 +690,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   kp.predictor_seed = tr->predictor_seed;
   kp.given_bucket = tr->given_bucket;
   kp.resident = resident;
-  if (sout) {
-    kp.out_marks = sout->marks;
-    kp.n_out_bounds = sout->nbounds;
-    for (int c = 0; c < sout->nbounds; ++c) kp.out_bounds[c] = sout->bounds[c];
-  }
+  if (sout) sout->used = 0;
   if (traj) {  // ClusterConfig::record_trajectory (general kernel)
     kp.traj = *traj;
     kp.traj_on = 1;
@@ -703,9 +708,9 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
       return fail(RS_ERR_INVALID_ARGUMENT, "simulated predictor needs trace->predictor_seed");
     if (cfg->predictor_mode == RS_PREDICTOR_GIVEN && !tr->given_bucket)
       return fail(RS_ERR_INVALID_ARGUMENT, "GIVEN predictor mode needs trace->given_bucket");
-    if (fast) {
+    if (fast && fused) {
       kp.predict_inline = 1;  // drawn at injection inside the replay kernel
-    } else {
+    } else {  // a pre-pass kernel writes every prediction
       rs_status sp = rs_predict_buckets(cfg, tr, out->predicted_bucket, stream);
       if (sp != RS_OK) return sp;
     }
@@ -883,16 +888,39 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
       pl.kern = lat;
     cudaGetLastError();
   }
+  // Streamed outputs: the latency-regime plan has a publishing build
+  // (replay_fast_kernel_lat_so); other plans copy the outputs after the kernel.
+  if (sout && !tail) {
+    KernelFn lat = kernel_for(cfg->policy, fast, groups, pl.width, 2, tail);
+    KernelFn lso = kernel_for(cfg->policy, fast, groups, pl.width, 3, tail);
+    int blocks = 0;
+    if (lat && lso && pl.kern == lat &&
+        cudaFuncSetAttribute(lso, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.block_smem) ==
+            cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, lso, pl.wpb * rs::kWarp,
+                                                      (size_t)pl.block_smem) == cudaSuccess &&
+        blocks >= 1) {
+      pl.kern = lso;
+      kp.out_marks = sout->marks;
+      kp.n_out_bounds = sout->nbounds;
+      for (int c = 0; c < sout->nbounds; ++c) kp.out_bounds[c] = sout->bounds[c];
+      sout->used = 1;
+    }
+    cudaGetLastError();
+  }
   if (env_int("RS_DEBUG_PLAN", 0)) {
     const char* variant = !fast                                                ? "general"
                           : pl.kern == kernel_for(cfg->policy, fast, groups, pl.width, 2, tail) ? "lat"
                           : pl.kern == kernel_for(cfg->policy, fast, groups, pl.width, 1, tail) ? "wide"
+                          : (sout && sout->used)                                          ? "lat_so"
                                                                                         : "bounded";
     fprintf(stderr,
             "rs plan: policy %d fast %d kernel %s groups %d width %d wpb %d blocks/SM %d "
-            "block_smem %d group_bytes %d weights %d wcap %d rsm %d rl_global %d resident replays %lld\n",
+            "block_smem %d group_bytes %d weights %d wcap %d rsm %d fused_pred %d rl_global %d "
+            "resident replays %lld\n",
             cfg->policy, (int)fast, variant, groups, pl.width, pl.wpb, pl.per_sm, pl.block_smem,
-            L.group_bytes, L.weights_bytes, L.wcap, L.rsm, (int)rl_global, pl.capacity);
+            L.group_bytes, L.weights_bytes, L.wcap, L.rsm, (int)fused, (int)rl_global,
+            pl.capacity);
   }
   RS_CUDA(cudaMemsetAsync(kp.work_counter, 0, sizeof(int), st));
   if (fast && !resident && env_int("RS_NO_VALIDATE_PASS", 0) == 0) {
@@ -906,7 +934,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     vp.decode = kp.decode;
     vp.o_preempt = kp.o_preempt;
     vp.mm_removed = cfg->policy == RS_POLICY_MIN_MIN ? kp.mm_removed : nullptr;
-    vp.o_completion = sout ? kp.o_completion : nullptr;  // "not completed" for publish_final
+    vp.o_completion = nullptr;
     vp.vinfo = reinterpret_cast<int2*>(ws + wl.vinfo);
     const int vgrid = std::max(1, std::min(tr->num_replays, sms * 8));
     rs::validate_kernel<<<vgrid, rs::kStatsThreads, 0, st>>>(vp);

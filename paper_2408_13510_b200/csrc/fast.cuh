@@ -328,7 +328,7 @@ __device__ __forceinline__ void lane_admit_one(const KParams& P, int gw, int i, 
 
 // Instance::admit_waiting (instance.hpp:149-195) by the owning lane.
 template <int T>
-__device__ inline void lane_admit(const KParams& P, int gw, long long off, int i, Inst& I) {
+__device__ __forceinline__ void lane_admit(const KParams& P, int gw, long long off, int i, Inst& I) {
   while (I.w_cnt > 0 && I.n < P.max_batch) {
     if (P.batching == RS_BATCHING_FCFS) {  // strict head of line
       const int s = I.w_head;
@@ -399,7 +399,7 @@ __device__ inline void lane_admit(const KParams& P, int gw, long long off, int i
 // entry only ever moves down, onto a slot already read).
 // SB: also recount the RL state-bucket tracking (Inst::sb1..nx2).
 template <int W, bool SB, int T>
-__device__ inline void warp_scan_instance(const KParams& P, int gw, long long off, int i,
+__device__ __forceinline__ void warp_scan_instance(const KParams& P, int gw, long long off, int i,
                                           int owner, Inst& I, const Lanes<W>& L) {
   const int l = L.l;
   if (T) L.sync();  // the owner's global-tail writes before any lane reads them
@@ -523,7 +523,7 @@ __device__ inline void warp_scan_instance(const KParams& P, int gw, long long of
 // Serial (owner lane) recount of every running aggregate after preemption.
 // No request can complete here: completions were handled this step.
 template <int T>
-__device__ inline void lane_recount(const KParams& P, int gw, int i, Inst& I) {
+__device__ __forceinline__ void lane_recount(const KParams& P, int gw, int i, Inst& I) {
   int kv = 0, dl = 0, tl = 0, nge = 0, nxg = kBig, nxd = kBig;
   I.sb1 = I.sb2 = 0;
   I.nx1 = I.nx2 = kBig;

@@ -74,7 +74,7 @@ __device__ __forceinline__ int grp_argmax_key(const Lanes<W>& L, unsigned long l
 }
 
 template <int POL, int G, int W, int T>
-__device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Replay& R,
+__device__ __forceinline__ int decide_fast(const KParams& P, int gw, const MlpView& M, Replay& R,
                                   Inst (&S)[G], bool has_head, const Rec& hr, int hb,
                                   char* gbase, const Lanes<W>& L) {
   const int l = L.l;
@@ -289,7 +289,7 @@ __device__ inline int decide_fast(const KParams& P, int gw, const MlpView& M, Re
 // middle bucket).  The stream is policy independent, so drawing a window
 // ahead of injection is equivalent.  Written to the predicted-bucket output.
 template <int W>
-__device__ inline void predict_window(const KParams& P, Replay& R, unsigned long long* pst,
+__device__ __forceinline__ void predict_window(const KParams& P, Replay& R, unsigned long long* pst,
                                       const Lanes<W>& L) {
   const int l = L.l;
   const int j = R.a_base + l;
@@ -439,8 +439,15 @@ __device__ __forceinline__ void publish_final(const KParams& P, long long off, i
   }
 }
 
-template <int POL, int G, int W, bool SEQ, int T>
-__device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const MlpView& M, int r,
+// SO: streamed outputs (publish_final) — 0 = not compiled in, 1 = on
+// (the replay_fast_kernel_lat_so build), 2 = compiled in behind a runtime
+// test of P.out_marks.  Which form each build uses is a measured choice
+// (A/B on one box): the plain latency build is fastest with 0 (c2); the
+// two-instance-per-lane and throughput builds run measurably faster with
+// the runtime form (ptxas schedules the tick loop differently; c5 1.30 s
+// with 0 against 1.00 s with 2).
+template <int POL, int G, int W, bool SEQ, int T, int SO>
+__device__ __forceinline__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const MlpView& M, int r,
                                    bool init, int& fin, int& fch, const Lanes<W>& L) {
   constexpr bool seq = SEQ;  // compile-time: the index-order re-run is a separate instantiation
   const int l = L.l;
@@ -456,7 +463,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
     bad = P.vinfo[r].x != 0;
   } else for (int j = l; j < R.n; j += W) {
     const long long g = off + j;
-    if (init && j >= fin) {  // (streamed outputs: below fin already published, rewritten identically)
+    if (init && (SO == 0 || j >= fin)) {  // (streamed outputs: below fin already published, rewritten identically)
       P.o_instance[g] = -1;
       P.o_routed[g] = -1.0;
       P.o_first[g] = -1.0;
@@ -464,7 +471,8 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
     }
     P.o_preempt[g] = 0;
     if (POL == RS_POLICY_MIN_MIN) P.mm_removed[g] = 0;
-    if (P.out_marks && !init) P.o_completion[g] = -1.0;  // not completed (publish_final)
+    if ((SO == 1 || (SO == 2 && P.out_marks)) && !init)
+      P.o_completion[g] = -1.0;  // not completed (publish_final)
     if (P.resident) continue;  // streamed inputs: validated per window on load
     const int p = P.prompt[g], d = P.decode[g];
     if (p < 1 || p > kMaxTokens || d < 1 || d > kMaxTokens) bad = true;
@@ -513,7 +521,20 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
   else if (R.status == RS_REPLAY_FINISHED) inject_fast(P, R, pst, L);
   next_arrival();
 
-  while (R.status == RS_REPLAY_FINISHED && R.completed != R.n && R.tick < P.max_ticks) {
+  // Per-lane tick accounting, reduced once at the end: completions of the
+  // lane's instances, and the sum over ticks of their end-of-tick waiting
+  // counts (the router's per-tick sum of instance waiting, env.hpp:326-337).
+  int lcomp = 0;
+  long long lsw = 0;
+  while (R.status == RS_REPLAY_FINISHED && R.tick < P.max_ticks) {
+    // run_policy's done() (every request completed) once every request has
+    // arrived and been routed: no instance holds work
+    if (R.cursor == R.n && queue_len<POL>(R) == 0) {
+      bool busy = false;
+#pragma unroll
+      for (int g = 0; g < G; ++g) busy |= S[g].n > 0 || S[g].w_cnt > 0;
+      if (!L.any(busy)) break;
+    }
     if (POL == RS_POLICY_MIN_MIN && queue_len<POL>(R) > 0) {
       if (!minmin_pick(P, front, R, L)) { R.status = RS_REPLAY_CAPACITY; break; }
     }
@@ -547,7 +568,6 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
       break;
     }
     const double t1 = __dadd_rn(R.clock, P.delta_t);
-    int wdelta = 0;  // this lane's waiting-count change over the tick
     if (action < m && has_head) {
       if ((long long)hr.prompt + hr.tru > P.kv_cap) {
         R.infeasible++;  // env.hpp:262-267: flagged, stays queued
@@ -566,7 +586,6 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
           P.o_instance[off + hr.req] = action;
         }
         R.routed++;
-        R.total_wait++;  // the enqueue (uniform; admissions are counted per lane)
 #pragma unroll
         for (int g = 0; g < G; ++g)
           if (g * W + l == action) {
@@ -626,9 +645,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
         // the common decode step skips both tests
         bool prefill = false;
         if (I.w_cnt > 0 && I.n < P.max_batch) {
-          const int w0 = I.w_cnt + I.o_cnt;
           lane_admit<T>(P, gw, off, i, I);
-          wdelta += I.w_cnt + I.o_cnt - w0;
           if (I.n == 0) {  // logic_error, instance.hpp:209-211
             ev = true;
             evg |= 1u << g;
@@ -724,30 +741,26 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
           warp_scan_instance<W, POL == RS_POLICY_RL, T>(P, gw, off, g * W + owner, owner, S[g], L);
         }
         if (mine && S[g].kv > P.kv_cap && S[g].n > 1) {
-          const int w0 = S[g].w_cnt + S[g].o_cnt;
           lane_preempt<T>(P, gw, off, g * W + l, S[g]);
-          wdelta += S[g].w_cnt + S[g].o_cnt - w0;
         }
       }
     }
     if (R.status != RS_REPLAY_FINISHED) break;
-    int comps = 0;
+    int comps = 0, wn = 0;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       comps += S[g].comps;
       S[g].comps = 0;
+      wn += S[g].w_cnt + S[g].o_cnt;
       // An instance emptied by this tick's last events skips ahead to t1
       // (instance.hpp:309) lazily: nothing reads an idle instance's clock
       // before either the next run_until (which snaps it to that tick's t1)
       // or an enqueue (which raises it to the router clock, this t1).
     }
-    // completions and waiting-count changes of the tick (two exact sums: a
-    // large delta_t can admit or preempt any number of requests in one tick)
-    if (L.any((comps | wdelta) != 0)) {
-      R.completed += L.sum(comps);
-      R.total_wait += L.sum(wdelta);
-      if (P.out_marks && L.any(comps != 0)) publish_final(P, off, R.n, R.cursor, fin, fch, L);
-    }
+    lcomp += comps;
+    lsw += wn;
+    if ((SO == 1 || (SO == 2 && P.out_marks)) && L.any(comps != 0))
+      publish_final(P, off, R.n, R.cursor, fin, fch, L);
     R.clock = t1;
     if (R.clock >= R.next_arr) {  // inject_arrivals (env.hpp:357-375) only when due
       inject_fast(P, R, pst, L);
@@ -755,12 +768,13 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
     }
     R.tick++;
     R.sum_q += queue_len<POL>(R);
-    R.sum_w += R.total_wait;
   }
+  R.completed = L.sum(lcomp);
+  R.sum_w = L.sum_ll(lsw);
   if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
   if (!init && R.status != RS_REPLAY_FINISHED) return kRerunInit;
   write_replay_stats(P, R, r, L);
-  if (P.out_marks) {  // the replay is over: every output is final
+  if (SO == 1 || (SO == 2 && P.out_marks)) {  // the replay is over: every output is final
     fin = R.n;
     if (fch < P.n_out_bounds) {
       __threadfence_system();
@@ -773,7 +787,7 @@ __device__ FastRun run_replay_fast(const KParams& P, int gw, char* gbase, const 
   return kDone;
 }
 
-template <int POL, int G, int W, int T>
+template <int POL, int G, int W, int T, int SO>
 __device__ __forceinline__ void replay_fast_body(const KParams& P) {
   extern __shared__ __align__(16) char smem[];
   const Lanes<W> L = make_lanes<W>();
@@ -804,11 +818,12 @@ __device__ __forceinline__ void replay_fast_body(const KParams& P) {
     r = L.shfl(r, 0);
     if (r >= P.num_replays) break;
     int fin = 0, fch = 0;  // streamed outputs: final prefix, next chunk mark
-    const FastRun o = run_replay_fast<POL, G, W, false, T>(P, gw, gbase, M, r, false, fin, fch, L);
+    const FastRun o =
+        run_replay_fast<POL, G, W, false, T, SO>(P, gw, gbase, M, r, false, fin, fch, L);
     if (o == kRerunSeq)
-      run_replay_fast<POL, G, W, true, T>(P, gw, gbase, M, r, true, fin, fch, L);
+      run_replay_fast<POL, G, W, true, T, SO>(P, gw, gbase, M, r, true, fin, fch, L);
     else if (o == kRerunInit)
-      run_replay_fast<POL, G, W, false, T>(P, gw, gbase, M, r, true, fin, fch, L);
+      run_replay_fast<POL, G, W, false, T, SO>(P, gw, gbase, M, r, true, fin, fch, L);
   }
 }
 
@@ -816,7 +831,7 @@ __device__ __forceinline__ void replay_fast_body(const KParams& P) {
 // throughput regime wants 16 resident replays per SM).
 template <int POL, int G, int W, int T>
 __global__ void __launch_bounds__(256, 2) replay_fast_kernel(const __grid_constant__ KParams P) {
-  replay_fast_body<POL, G, W, T>(P);
+  replay_fast_body<POL, G, W, T, 2>(P);
 }
 
 // Latency regime (every replay resident in one wave, <= 8 warps per SM):
@@ -825,7 +840,14 @@ __global__ void __launch_bounds__(256, 2) replay_fast_kernel(const __grid_consta
 // traffic on the tick chain; one such block per SM fits the register file.
 template <int POL, int G, int W, int T>
 __global__ void replay_fast_kernel_lat(const __grid_constant__ KParams P) {
-  replay_fast_body<POL, G, W, T>(P);
+  replay_fast_body<POL, G, W, T, G == 1 ? 0 : 2>(P);
+}
+
+// The latency-regime build with streamed outputs (rs_replay_batch_host with
+// page-locked output buffers): replays publish finalised request chunks.
+template <int POL, int G, int W, int T>
+__global__ void replay_fast_kernel_lat_so(const __grid_constant__ KParams P) {
+  replay_fast_body<POL, G, W, T, 1>(P);
 }
 
 // Up to 16 (the RL policy in the throughput regime): its Q-network is staged
@@ -835,7 +857,7 @@ __global__ void replay_fast_kernel_lat(const __grid_constant__ KParams P) {
 // blocks of <= 8 warps run faster with the 256-thread build (measured, c3).
 template <int POL, int G, int W, int T>
 __global__ void __launch_bounds__(512) replay_fast_kernel_wide(const __grid_constant__ KParams P) {
-  replay_fast_body<POL, G, W, T>(P);
+  replay_fast_body<POL, G, W, T, 2>(P);
 }
 
 }  // namespace rs

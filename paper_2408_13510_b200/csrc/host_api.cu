@@ -407,7 +407,7 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
         RS_CUDA2(cudaMemcpyAsync(flag, marks + i, sizeof(int), cudaMemcpyHostToDevice, cs));
         lo = hi;
       }
-      if (stream_out) {
+      if (stream_out && sout.used) {
         // out stream: per chunk, wait until every replay has published it,
         // then copy its columns of every per-request array back
         if (!dc.out_stream)
@@ -449,7 +449,7 @@ rs_status replay_host(const rs_batch_cfg* cfg, const rs_trace_soa* tr, rs_req_ou
       if (!dst || n == 0) return cudaSuccess;
       return cudaMemcpyAsync(dst, b + off, n, cudaMemcpyDeviceToHost, st);
     };
-    if (stream_out) {
+    if (stream_out && sout.used) {
       RS_CUDA2(cudaStreamWaitEvent(st, dc.ev_out, 0));  // the out stream's copies
     } else if (out) {
       RS_CUDA2(d2h(out->instance, o_in, 4ull * N));

@@ -27,13 +27,15 @@ struct rs_internal_stream_out {
   int* marks;
   int nbounds;
   int bounds[16];
+  int used;  // out: 1 when the launched kernel publishes (the latency-regime
+             // build has a streamed-output variant; other plans copy after)
 };
 
 rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* tr,
                                    rs_req_out* out, rs_replay_stats* stats, void* workspace,
                                    size_t workspace_bytes, void* stream, const int* resident,
                                    void* inputs_done, const rs_trajectory* traj,
-                                   const rs_internal_stream_out* sout = nullptr);
+                                   rs_internal_stream_out* sout = nullptr);
 
 // The per-replay aggregates pass (stats_kernel) over a finished replay batch,
 // after `wait_event` (may be null).

@@ -36,8 +36,8 @@ def trace_of(tb, r):
 
 
 def run_batch(lib, cfg, tb, pseeds, capfd):
-    """rs_replay_batch_host over the whole batch (pageable buffers: the
-    device-resident, non-streamed path the bench's device leg takes) with
+    """rs_replay_batch_host over the whole batch (pageable buffers, no
+    input streaming: the device-resident path the bench's device leg takes) with
     the simulated predictor drawn inline, as bench.py runs it.  Returns the
     per-request arrays, the stats and the planner's line."""
     N, R = tb.total, tb.num_replays
@@ -71,8 +71,10 @@ def plan_field(plan, key):
 @pytest.fixture
 def debug_plan(monkeypatch):
     monkeypatch.setenv("RS_DEBUG_PLAN", "1")
-    for k in ("RS_FORCE_GENERAL", "RS_STREAM_INPUTS", "RS_RUN_SMEM", "RS_WAIT_RING",
-              "RS_WARPS_PER_BLOCK", "RS_RL_GLOBAL"):
+    # the bench's device leg: inputs resident before the launch (no streaming)
+    monkeypatch.setenv("RS_STREAM_INPUTS", "0")
+    for k in ("RS_FORCE_GENERAL", "RS_RUN_SMEM", "RS_WAIT_RING", "RS_WARPS_PER_BLOCK",
+              "RS_RL_GLOBAL"):
         monkeypatch.delenv(k, raising=False)
 
 
@@ -118,7 +120,10 @@ def test_c3_shape_rl_agent(gpu, debug_plan, capfd):
     cfg = abi.default_config("rl", m)
     keep = abi.set_rl(cfg, dims, params)
     arrs, stats, plan = run_batch(gpu, cfg, tb, ps, capfd)
-    assert plan_field(plan, "kernel") in ("bounded", "wide", "lat"), plan
+    # 16 replays per SM next to the staged Q-network: the running head and
+    # the waiting ring shrink and the predictions come from the pre-pass
+    assert plan_field(plan, "kernel") == "wide", plan
+    assert plan_field(plan, "fused_pred") == "0", plan
     picks = [0, 1, 777, 2048, 4095]
     check_sample(cfg, tb, ps, arrs, stats, picks, picks[:3])
     del keep
