@@ -109,6 +109,7 @@ struct KParams {
   // shared-memory layout (bytes, per replay group)
   int smem_group_bytes;
   int off_run, off_wait, off_dbc, off_rlx, off_rng, off_front;
+  int off_pair;  // warp-pair exchange words (pair.cuh), bytes
   // fast kernel: word offsets (relative to the group base) of the running
   // entry fields and waiting-ring fields, per-instance running stride, and
   // the power-of-two lane width covering the instances (argmin reductions)

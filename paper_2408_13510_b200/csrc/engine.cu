@@ -67,7 +67,7 @@ rs_status require_device() {
 // Smem layout of one replay group (one warp) for this config.
 struct Layout {
   int rcap, rsm, wcap;
-  int off_run, off_wait, off_dbc, off_rlx, off_rng, off_front, off_pred, group_bytes;
+  int off_run, off_wait, off_dbc, off_rlx, off_rng, off_front, off_pred, off_pair, group_bytes;
   int weights_bytes;
   int woff[RS_MAX_LAYERS], boff[RS_MAX_LAYERS];
   int maxw;
@@ -126,6 +126,8 @@ Layout make_layout(const rs_batch_cfg& c, int wcap, bool fast, int rsm = 0, bool
   if (fast && fused && (c.flags & RS_FLAG_PREDICT_INLINE) &&
       c.predictor_mode == RS_PREDICTOR_SIMULATED)
     off = align_up(off + 312 * sizeof(unsigned long long), 16);
+  L.off_pair = (int)off;  // warp-pair exchange words (m > 32: pair.cuh)
+  if (fast && m > 32) off = align_up(off + 32 * sizeof(int), 16);
   L.group_bytes = (int)align_up(off, 128);
   L.weights_bytes = 0;
   if (rl) {
@@ -245,7 +247,8 @@ size_t run_tail_ints(const rs_batch_cfg& c, int64_t num_replays) {
   if (c.chunk_size != 0 || c.num_instances > 64 || rcap <= 1) return 0;
   // (a launch may round the replay count up to whole blocks of <= 16 warps,
   // and any warp can take any replay from the work counter)
-  const int64_t warps = std::min<int64_t>(num_replays + 16, (int64_t)sm_count() * 64);
+  // (two warps per replay for m > 32: pair.cuh)
+  const int64_t warps = std::min<int64_t>(2 * num_replays + 32, (int64_t)sm_count() * 64);
   return (size_t)warps * 5 * c.num_instances * (rcap - 1);
 }
 
@@ -687,6 +690,7 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
   kp.off_rng = L.off_rng;
   kp.off_front = L.off_front;
   kp.off_pred = L.off_pred;
+  kp.off_pair = L.off_pair;
   kp.predictor_seed = tr->predictor_seed;
   kp.given_bucket = tr->given_bucket;
   kp.resident = resident;
@@ -941,9 +945,45 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     RS_CUDA(cudaGetLastError());
     kp.vinfo = vp.vinfo;
   }
-  rs_status s2 = launch_kernel(pl.kern, kp, pl.wpb, rs::kWarp / pl.width, pl.block_smem,
-                               tr->num_replays, st);
-  if (s2 != RS_OK) return s2;
+  // Fleets of 33..64 instances: two warps per replay, one instance per lane
+  // (pair.cuh), when the heuristic has a pair build.  Pairs per block: all
+  // replays resident in one wave when they fit, <= 8 pairs (16 warps) per
+  // block.
+  KernelFn pk = nullptr;
+  int ppb = 0, pair_blocks = 0;
+  if (fast && groups == 2 && !(sout && sout->used) && !traj &&
+      env_int("RS_NO_PAIR", 0) == 0)
+    pk = kernel_for(cfg->policy, fast, groups, rs::kWarp, 4, tail);
+  if (pk) {
+    const int want = std::max(1, std::min(8, (tr->num_replays + sms - 1) / sms));
+    for (ppb = want; ppb >= 1; --ppb) {
+      const int bytes = ppb * L.group_bytes;
+      if (bytes > smem_optin) continue;
+      if (cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) !=
+              cudaSuccess ||
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pair_blocks, pk, 64 * ppb,
+                                                        (size_t)bytes) != cudaSuccess) {
+        cudaGetLastError();
+        pair_blocks = 0;
+        continue;
+      }
+      if (pair_blocks >= 1) break;
+    }
+    if (ppb < 1 || pair_blocks < 1) pk = nullptr;
+  }
+  if (pk) {
+    if (env_int("RS_DEBUG_PLAN", 0))
+      fprintf(stderr, "rs plan: policy %d fast 1 kernel pair pairs/block %d blocks/SM %d "
+              "group_bytes %d wcap %d rsm %d\n", cfg->policy, ppb, pair_blocks, L.group_bytes,
+              L.wcap, L.rsm);
+    const int grid = std::max(1, std::min((tr->num_replays + ppb - 1) / ppb, sms * pair_blocks));
+    pk<<<grid, 64 * ppb, ppb * L.group_bytes, st>>>(kp);
+    RS_CUDA(cudaGetLastError());
+  } else {
+    rs_status s2 = launch_kernel(pl.kern, kp, pl.wpb, rs::kWarp / pl.width, pl.block_smem,
+                                 tr->num_replays, st);
+    if (s2 != RS_OK) return s2;
+  }
   // compute_metrics aggregates (metrics.hpp:62-162), one CTA per replay;
   // the streamed-input caller launches them itself once its copies are queued
   if (inputs_done == kDeferStats) return RS_OK;

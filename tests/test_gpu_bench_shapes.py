@@ -169,7 +169,7 @@ def test_c5_shape_large_fleet(gpu, debug_plan, capfd):
     ps = np.concatenate([bps, sps])
     cfg = abi.default_config("workload_aware", m)
     arrs, stats, plan = run_batch(gpu, cfg, tb, ps, capfd)
-    assert plan_field(plan, "groups") == "2", plan
+    assert plan_field(plan, "kernel") == "pair", plan  # two warps per replay (pair.cuh)
     check_sample(cfg, tb, ps, arrs, stats, [0, 1, 2, 300, R - 1], [2, R - 1])
 
 

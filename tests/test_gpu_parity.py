@@ -281,3 +281,31 @@ def test_streamed_inputs_validate_per_window(gpu, kernel_path):
     assert got[1].stats["status"][0] == abi.REPLAY_INVALID_TRACE
     assert got[2].stats["status"][0] == abi.REPLAY_INVALID_TRACE
 
+
+
+@pytest.mark.parametrize("m", [40, 64])
+def test_large_fleets_warp_pairs_and_reruns(gpu, kernel_path, m, monkeypatch):
+    """33..64 instances: the warp-pair kernel (pair.cuh; "fast" and "tail"
+    paths), the two-instances-per-lane kernel (RS_NO_PAIR, and the streamed
+    path), every heuristic pair build, and the pair kernel's re-runs on the
+    single-warp code: "nothing admissible" (index-order re-run) and
+    max_ticks (re-run with output initialisation)."""
+    if kernel_path == "general":
+        pytest.skip("fast-kernel plans only")
+    for no_pair in ("0", "1"):
+        monkeypatch.setenv("RS_NO_PAIR", no_pair)
+        tb = engine.build_workload(range(60, 64), 1800, 30.0)
+        traces = [O.Trace(tb.arrival[tb.replay(r)], tb.prompt[tb.replay(r)],
+                          tb.decode[tb.replay(r)], tb.task[tb.replay(r)]) for r in range(4)]
+        ps = [abi.mix_seed(s, 0x9DED) for s in range(60, 64)]
+        cases = [(pol, {}) for pol in sorted(abi.POLICIES.keys() - {"rl", "min_min"})]
+        cases += [("jsq", {"kv_capacity_tokens": 4096}),            # nothing admissible
+                  ("round_robin", {"kv_capacity_tokens": 4096, "max_ticks": 20000})]  # unfinished
+        for pol, over in cases:
+            cfg = abi.default_config(pol, m)
+            for k, v in over.items():
+                setattr(cfg, k, v)
+            got = run_engine(gpu, cfg, traces, ps)
+            for r, tr in enumerate(traces):
+                want = O.ora_run(cfg, tr, ps[r])
+                assert O.compare(got[r], want) == [], (no_pair, pol, over, r)
