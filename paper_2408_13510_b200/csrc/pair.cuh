@@ -17,9 +17,11 @@
 //     with the lower instance index winning ties, exactly the whole-fleet
 //     order of policies.hpp);
 //   * the fused predictor's draws (warp 0 draws, the barrier publishes them);
-//   * one barrier reduction per tick (bar.red.or): "nothing admissible"
-//     anywhere in the fleet, and run_policy's done() once every request has
-//     arrived and been routed;
+//   * "nothing admissible" flags, carried by the decision exchanges (every
+//     tick with a head) and by the barrier reductions (bar.red.or) of
+//     run_policy's done() once every request has arrived and been routed —
+//     between those the warps may be a few ticks apart, which nothing
+//     observes (disjoint instances, replicated replay state);
 //   * the final completion / waiting sums.
 // Instance stepping and its events (admission, prefill, decode steps,
 // completion scans, preemption) touch only the warp's own instances and run
@@ -54,28 +56,38 @@ __device__ __forceinline__ bool pair_any(const Pair& Q, bool p) {
       : "memory");
   return r != 0;
 }
-// Each warp posts three words (lane 0), the other warp's come back.
+// Each warp posts three words and its error flag (lane 0); the other
+// warp's come back, the flags OR-ed into `err`.
 __device__ __forceinline__ void pair_swap3(Pair& Q, int l, int a, int b, int c, int& oa, int& ob,
-                                           int& oc) {
+                                           int& oc, bool own_err, bool& err) {
   int* x = Q.xw + Q.bank * 8;
   Q.bank ^= 1;
   if (l == 0) {
     x[Q.wid * 4 + 0] = a;
     x[Q.wid * 4 + 1] = b;
     x[Q.wid * 4 + 2] = c;
+    x[Q.wid * 4 + 3] = own_err;
   }
   pair_sync(Q);
   const int o = (Q.wid ^ 1) * 4;
   oa = x[o];
   ob = x[o + 1];
   oc = x[o + 2];
+  err = err || own_err || x[o + 3] != 0;
 }
 
 // The routing decision of decide_fast for the whole fleet, from each warp's
-// half: the same scores per instance, combined in index order.
+// half: the same scores per instance, combined in index order.  The
+// exchange also carries the warps' "nothing admissible" flags (`err`, in:
+// this warp's; out: either's when an exchange took place, else false — a
+// decision without an exchange is made by both warps alone); the caller
+// re-runs the replay when it comes back set.
 template <int POL>
 __device__ __forceinline__ int decide_pair(const KParams& P, Replay& R, Inst& I, bool has_head,
-                                           const Rec& hr, const Lanes<kWarp>& L, Pair& Q) {
+                                           const Rec& hr, const Lanes<kWarp>& L, Pair& Q,
+                                           bool& err) {
+  const bool own_err = err;
+  err = false;
   const int l = L.l;
   const int m = P.m;
   const int i = Q.wid * kWarp + l;
@@ -93,7 +105,7 @@ __device__ __forceinline__ int decide_pair(const KParams& P, Replay& R, Inst& I,
     const bool mine = (t >> 5) == Q.wid;
     int ok = mine ? L.shfl((int)(i == t && can_accept(P, feat_of(I), need)), t & (kWarp - 1)) : 0;
     int ook, d1, d2;
-    pair_swap3(Q, l, ok, 0, 0, ook, d1, d2);
+    pair_swap3(Q, l, ok, 0, 0, ook, d1, d2, own_err, err);
     if (!mine) ok = ook;
     if (!ok) return m;
     if (POL == RS_POLICY_ROUND_ROBIN) R.rr_next++;
@@ -103,7 +115,7 @@ __device__ __forceinline__ int decide_pair(const KParams& P, Replay& R, Inst& I,
     const bool ok = here && (long long)P.kv_cap - feat_of(I).res >= need;
     const int b = (int)L.ballot(ok);
     int ob, d1, d2;
-    pair_swap3(Q, l, b, 0, 0, ob, d1, d2);
+    pair_swap3(Q, l, b, 0, 0, ob, d1, d2, own_err, err);
     const unsigned b0 = (unsigned)(Q.wid == 0 ? b : ob), b1 = (unsigned)(Q.wid == 0 ? ob : b);
     if (b0) return __ffs(b0) - 1;
     if (b1) return kWarp + __ffs(b1) - 1;
@@ -114,7 +126,7 @@ __device__ __forceinline__ int decide_pair(const KParams& P, Replay& R, Inst& I,
     const int a = grp_argmax_key(L, k, here);
     const unsigned long long ka = a >= 0 ? L.shfl(k, a) : 0ull;
     int hi, lo, oi;
-    pair_swap3(Q, l, (int)(ka >> 32), (int)ka, a >= 0 ? Q.wid * kWarp + a : -1, hi, lo, oi);
+    pair_swap3(Q, l, (int)(ka >> 32), (int)ka, a >= 0 ? Q.wid * kWarp + a : -1, hi, lo, oi, own_err, err);
     const unsigned long long ko = ((unsigned long long)(unsigned)hi << 32) | (unsigned)lo;
     const int mi = a >= 0 ? Q.wid * kWarp + a : -1;
     // index order: warp 0's best, replaced only by a strictly larger key
@@ -127,7 +139,7 @@ __device__ __forceinline__ int decide_pair(const KParams& P, Replay& R, Inst& I,
                            bi & (kWarp - 1))
                   : 0;
     int ook, d1, d2;
-    pair_swap3(Q, l, ok, 0, 0, ook, d1, d2);
+    pair_swap3(Q, l, ok, 0, 0, ook, d1, d2, own_err, err);
     if (!mine) ok = ook;
     if (!ok) return m;
     R.mc_next = __dadd_rn(R.clock, 1.0);
@@ -161,7 +173,7 @@ __device__ __forceinline__ int decide_pair(const KParams& P, Replay& R, Inst& I,
     const int a = argmin_narrow(L, k, v, kWarp);
     const unsigned long long ka = a >= 0 ? L.shfl(k, a) : ~0ull;
     int hi, lo, oi;
-    pair_swap3(Q, l, (int)(ka >> 32), (int)ka, a >= 0 ? Q.wid * kWarp + a : -1, hi, lo, oi);
+    pair_swap3(Q, l, (int)(ka >> 32), (int)ka, a >= 0 ? Q.wid * kWarp + a : -1, hi, lo, oi, own_err, err);
     const unsigned long long ko = ((unsigned long long)(unsigned)hi << 32) | (unsigned)lo;
     const int mi = a >= 0 ? Q.wid * kWarp + a : -1;
     const int i0 = Q.wid == 0 ? mi : oi, i1 = Q.wid == 0 ? oi : mi;
@@ -305,6 +317,7 @@ __device__ __forceinline__ FastRun run_replay_pair(const KParams& P, int gw, cha
   bool perr = false;  // "nothing admissible" in this warp's half
   while (R.status == RS_REPLAY_FINISHED && R.tick < P.max_ticks) {
     if (R.cursor == R.n && queue_len<POL>(R) == 0) {  // run_policy's done()
+      if (pair_any(Q, perr)) return kRerunSeq;
       if (!pair_any(Q, i < m && (I.n > 0 || I.w_cnt > 0))) break;
     }
     const bool has_head = queue_len<POL>(R) > 0;
@@ -327,7 +340,9 @@ __device__ __forceinline__ FastRun run_replay_pair(const KParams& P, int gw, cha
     } else {
       hr.req = hr.prompt = hr.dhat = hr.tru = hr.emit = 0;
     }
-    const int action = decide_pair<POL>(P, R, I, has_head, hr, L, Q);
+    bool err = perr;
+    const int action = decide_pair<POL>(P, R, I, has_head, hr, L, Q, err);
+    if (err) return kRerunSeq;  // (both warps: the flag came through the exchange)
     R.hash = hash_action(R.hash, action);
     const double t1 = __dadd_rn(R.clock, P.delta_t);
     if (action < m && has_head) {
@@ -346,7 +361,9 @@ __device__ __forceinline__ FastRun run_replay_pair(const KParams& P, int gw, cha
 
     // ---- run_until(t1) of this warp's instances (warp-local) ------------
     bool act = false;
-    if (i < m && I.clock < t1) {
+    // (a warp that hit "nothing admissible" stops stepping; the replay is
+    // re-run at the pair's next exchange)
+    if (!perr && i < m && I.clock < t1) {
       if (I.n > 0 || I.w_cnt > 0) act = true;
       else I.clock = t1;  // idle instance skips ahead (instance.hpp:309)
     }
@@ -427,8 +444,6 @@ __device__ __forceinline__ FastRun run_replay_pair(const KParams& P, int gw, cha
       }
       if (ev && I.kv > P.kv_cap && I.n > 1) lane_preempt<T>(P, gw, off, i, I);
     }
-    // one barrier per tick: the whole fleet's error flag
-    if (pair_any(Q, perr)) return kRerunSeq;
     lcomp += I.comps;
     I.comps = 0;
     lsw += I.w_cnt + I.o_cnt;
@@ -440,11 +455,13 @@ __device__ __forceinline__ FastRun run_replay_pair(const KParams& P, int gw, cha
     R.tick++;
     R.sum_q += queue_len<POL>(R);
   }
+  if (pair_any(Q, perr)) return kRerunSeq;
   // fleet totals: each warp's sums, exchanged
   const int c = L.sum(lcomp);
   const long long w = L.sum_ll(lsw);
   int oc, ohi, olo;
-  pair_swap3(Q, l, c, (int)(w >> 32), (int)w, oc, ohi, olo);
+  bool nerr = false;
+  pair_swap3(Q, l, c, (int)(w >> 32), (int)w, oc, ohi, olo, false, nerr);
   R.completed = c + oc;
   R.sum_w = w + (long long)(((unsigned long long)(unsigned)ohi << 32) | (unsigned)olo);
   if (R.status == RS_REPLAY_FINISHED && R.completed != R.n) R.status = RS_REPLAY_MAX_TICKS;
