@@ -200,19 +200,21 @@ def sample_plan(cfgname, per):
             for pi, policy in enumerate(pols)]
 
 
-def cpu_reference(cfgname, sample_replays, threads):
+def cpu_reference(cfgname, sample_replays, threads, noscan=False):
     """Compiled unmodified reference (oracle/_ref) on host threads over the
     bounded sample of sample_plan: traces from the reference's own generator
     (build_workload, experiment.hpp:291-305, via ref_generate_mixture), the
     agent from its own DqnAgent constructor, replays through its own
     ClusterSim::run_policy.  Nothing of the engine is loaded on this path.
     Returns (decisions/s, decisions, wall s, description, samples) with
-    samples = [(policy, rate_index, seed, rs_replay_stats record)]."""
+    samples = [(policy, rate_index, seed, rs_replay_stats record)].
+    noscan: the reference with its reward-only per-tick queue-penalty scan
+    (env.hpp:289-298) compiled out (oracle/Makefile, librs_ref_noscan.so)."""
     sys.path.insert(0, str(ROOT / "tests"))
     import oracles as O  # baseline infrastructure
     from paper_2408_13510_b200 import abi  # ctypes structs only (no library load)
     n, R, m, rates, pols, weights, desc = cfg_shape(cfgname)
-    lib = O.ref_lib()
+    lib = O.ref_lib(noscan=noscan)
     per = max(1, sample_replays)  # one replay per host thread, per policy
     ticks = 0
     wall = 0.0
@@ -681,13 +683,26 @@ def main():
                                         "kind": "reference", "sample": f"unavailable: {e}"}
         if world == 1:
             try:
-                pv, pticks, pwall = cpu_port_scan_free(args.config, sample, threads)
+                # like for like: the same reference with its reward-only
+                # per-tick scan (env.hpp:289-298) compiled out, the work the
+                # engine does
+                pv, pticks, pwall, _, _ = cpu_reference(args.config, sample, threads,
+                                                        noscan=True)
                 line["cpu_baseline_scan_free"] = {
-                    "value": pv, "unit": UNIT, "cores": threads, "kind": "port",
-                    "sample": f"same sample, oracle/rs_oracle.c (no per-tick reward scan), "
+                    "value": pv, "unit": UNIT, "cores": threads,
+                    "kind": "reference (patched: env.hpp:289-298 reward scan compiled out)",
+                    "sample": f"same sample, oracle/_ref/librs_ref_noscan.so, "
                               f"{pwall:.1f} s wall, {pticks} decisions"}
             except Exception as e:
                 line["cpu_baseline_scan_free"] = {"value": None, "sample": f"unavailable: {e}"}
+            try:  # the plain-C restatement of the same scan-free tick loop
+                cv2, cticks2, cwall2 = cpu_port_scan_free(args.config, sample, threads)
+                line["cpu_baseline_c_port"] = {
+                    "value": cv2, "unit": UNIT, "cores": threads, "kind": "port",
+                    "sample": f"same sample, oracle/rs_oracle.c (no per-tick reward scan), "
+                              f"{cwall2:.1f} s wall, {cticks2} decisions"}
+            except Exception as e:
+                line["cpu_baseline_c_port"] = {"value": None, "sample": f"unavailable: {e}"}
     print(json.dumps(line), flush=True)
     del keep
     if world > 1:

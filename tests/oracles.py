@@ -23,6 +23,7 @@ from paper_2408_13510_b200 import abi
 ROOT = Path(__file__).resolve().parents[1]
 ORA_PATH = ROOT / "oracle" / "build" / "librs_oracle.so"
 REF_PATH = ROOT / "oracle" / "_ref" / "librs_ref.so"
+REF_NOSCAN_PATH = ROOT / "oracle" / "_ref" / "librs_ref_noscan.so"
 REFERENCE_DIR = Path(os.environ.get("RS_REFERENCE_DIR", "/root/reference"))
 
 
@@ -32,6 +33,7 @@ def _make(target: str) -> None:
 
 _ora = None
 _ref = None
+_ref_noscan = None
 
 
 def ora_lib() -> C.CDLL:
@@ -59,38 +61,49 @@ def have_ref() -> bool:
     return REF_PATH.exists() or (REFERENCE_DIR / "proj" / "include" / "routesim").exists()
 
 
-def ref_lib() -> C.CDLL:
-    global _ref
+def ref_lib(noscan: bool = False) -> C.CDLL:
+    """oracle/_ref/librs_ref.so (the unmodified reference); noscan=True: the
+    same with the reward-only queue-penalty scan compiled out (Makefile)."""
+    global _ref, _ref_noscan
+    if noscan:
+        if _ref_noscan is None:
+            if not REF_NOSCAN_PATH.exists():
+                _make("ref")
+            _ref_noscan = _declare_ref(C.CDLL(str(REF_NOSCAN_PATH)))
+        return _ref_noscan
     if _ref is None:
         if not REF_PATH.exists():
             _make("ref")
-        lib = C.CDLL(str(REF_PATH))
-        P = C.POINTER
-        lib.ref_generate_mixture.argtypes = [P(abi.Profile), P(abi.Thresholds), C.c_void_p,
-                                             C.c_uint64, C.c_int64, C.c_double, C.c_int32,
-                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
-        lib.ref_run_replay.argtypes = [P(abi.BatchCfg), C.c_int64] + [C.c_void_p] * 4 + [
-            C.c_uint64, C.c_uint64] + [C.c_void_p] * 8 + [C.c_int64]
-        lib.ref_run_trajectory.argtypes = [P(abi.BatchCfg), C.c_int64] + [C.c_void_p] * 4 + [
-            C.c_uint64, C.c_uint64] + [C.c_void_p] * 7 + [P(abi.Trajectory)]
-        lib.ref_run_batch.restype = C.c_double
-        lib.ref_run_batch.argtypes = [P(abi.BatchCfg), C.c_int32] + [C.c_void_p] * 7 + [
-            C.c_int32, C.c_void_p]
-        lib.ref_agent_init.restype = C.c_int64
-        lib.ref_agent_init.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p,
-                                       C.c_int64]
-        lib.ref_mlp_forward.argtypes = [P(abi.BatchCfg), C.c_void_p, C.c_int32, C.c_void_p,
-                                        C.c_void_p]
-        lib.ref_golden_summary.argtypes = [C.c_char_p, C.c_size_t, C.c_int32]
-        lib.ref_experiment_summary.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_uint64,
-                                               C.c_char_p, C.c_char_p, C.c_size_t]
-        lib.ref_mix_seed.restype = C.c_uint64
-        lib.ref_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
-        lib.ref_heavy_decode_cutoff.restype = C.c_int64
-        lib.ref_heavy_decode_cutoff.argtypes = [P(abi.Profile), P(abi.Thresholds)]
-        lib.ref_last_error.argtypes = [C.c_char_p, C.c_size_t]
-        _ref = lib
+        _ref = _declare_ref(C.CDLL(str(REF_PATH)))
     return _ref
+
+
+def _declare_ref(lib: C.CDLL) -> C.CDLL:
+    P = C.POINTER
+    lib.ref_generate_mixture.argtypes = [P(abi.Profile), P(abi.Thresholds), C.c_void_p,
+                                         C.c_uint64, C.c_int64, C.c_double, C.c_int32,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.ref_run_replay.argtypes = [P(abi.BatchCfg), C.c_int64] + [C.c_void_p] * 4 + [
+        C.c_uint64, C.c_uint64] + [C.c_void_p] * 8 + [C.c_int64]
+    lib.ref_run_trajectory.argtypes = [P(abi.BatchCfg), C.c_int64] + [C.c_void_p] * 4 + [
+        C.c_uint64, C.c_uint64] + [C.c_void_p] * 7 + [P(abi.Trajectory)]
+    lib.ref_run_batch.restype = C.c_double
+    lib.ref_run_batch.argtypes = [P(abi.BatchCfg), C.c_int32] + [C.c_void_p] * 7 + [
+        C.c_int32, C.c_void_p]
+    lib.ref_agent_init.restype = C.c_int64
+    lib.ref_agent_init.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_void_p,
+                                   C.c_int64]
+    lib.ref_mlp_forward.argtypes = [P(abi.BatchCfg), C.c_void_p, C.c_int32, C.c_void_p,
+                                    C.c_void_p]
+    lib.ref_golden_summary.argtypes = [C.c_char_p, C.c_size_t, C.c_int32]
+    lib.ref_experiment_summary.argtypes = [C.c_int32, C.c_int64, C.c_double, C.c_uint64,
+                                           C.c_char_p, C.c_char_p, C.c_size_t]
+    lib.ref_mix_seed.restype = C.c_uint64
+    lib.ref_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
+    lib.ref_heavy_decode_cutoff.restype = C.c_int64
+    lib.ref_heavy_decode_cutoff.argtypes = [P(abi.Profile), P(abi.Thresholds)]
+    lib.ref_last_error.argtypes = [C.c_char_p, C.c_size_t]
+    return lib
 
 
 def ref_error() -> str:

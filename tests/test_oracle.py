@@ -123,3 +123,28 @@ def test_mlp_forward_matches_reference():
         assert np.array_equal(q1.view(np.uint64), q2.view(np.uint64))
         assert np.array_equal(g1, g2)
         del keep
+
+
+def test_patched_reference_without_reward_scan_matches():
+    """oracle/_ref/librs_ref_noscan.so (the reference with the reward-only
+    queue-penalty scan compiled out) replays to the same
+    statistics as the unmodified reference: the scan feeds no decision."""
+    if not O.have_ref():
+        pytest.skip("reference sources not available")
+    for pol, m, seed in (("workload_aware", 4, 3), ("jsq", 8, 4), ("round_robin", 2, 5)):
+        tr = O.ref_generate(seed, 1500, 25.0)
+        cfg = abi.default_config(pol, m)
+        ps = abi.mix_seed(seed, 0x9DED)
+        stats = []
+        for noscan in (False, True):
+            lib = O.ref_lib(noscan=noscan)
+            off = np.array([0, tr.arrival.size], np.int64)
+            st = np.zeros(1, abi.STATS_DTYPE)
+            psa = np.array([ps], np.uint64)
+            w = lib.ref_run_batch(C.byref(cfg), 1, off.ctypes.data, tr.arrival.ctypes.data,
+                                  tr.prompt.ctypes.data, tr.decode.ctypes.data,
+                                  tr.task.ctypes.data, psa.ctypes.data, None, 1,
+                                  st.ctypes.data)
+            assert w > 0
+            stats.append(st)
+        assert stats[0].tobytes() == stats[1].tobytes(), pol
