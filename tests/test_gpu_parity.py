@@ -309,3 +309,34 @@ def test_large_fleets_warp_pairs_and_reruns(gpu, kernel_path, m, monkeypatch):
             for r, tr in enumerate(traces):
                 want = O.ora_run(cfg, tr, ps[r])
                 assert O.compare(got[r], want) == [], (no_pair, pol, over, r)
+
+
+@pytest.mark.parametrize("m", [4, 8, 40])
+def test_no_head_windows_match_oracle(gpu, kernel_path, m, monkeypatch):
+    """No-head windows (fast_kernel.cuh / pair.cuh): the ticks between an
+    empty router queue and the next arrival run as one run_until.  Sparse
+    arrivals (long windows), tick lengths below and above a decode step (one
+    step crossing several boundaries: each must add the waiting count of the
+    state before the next step), max_ticks falling inside a window, and
+    bin-packing admission (waiting queues that persist through a window)."""
+    if kernel_path == "general" and m > 32:
+        pytest.skip("general kernel: covered at m <= 32")
+    monkeypatch.setenv("RS_NO_PAIR", "0")
+    tb = engine.build_workload(range(80, 84), 700, 3.0 if m <= 8 else 12.0)
+    traces = [O.Trace(tb.arrival[tb.replay(r)], tb.prompt[tb.replay(r)],
+                      tb.decode[tb.replay(r)], tb.task[tb.replay(r)]) for r in range(4)]
+    ps = [abi.mix_seed(s, 0x9DED) for s in range(80, 84)]
+    cases = [("workload_aware", {}), ("jsq", {"delta_t": 0.005}),
+             ("round_robin", {"delta_t": 0.0931}), ("earliest_available", {"delta_t": 0.3}),
+             ("decode_balancer", {"max_ticks": 5003}),
+             ("workload_aware", {"delta_t": 0.05, "max_ticks": 1777}),
+             ("max_capacity", {"batching": abi.BATCHING["bin_packing"], "kv_capacity_tokens": 6000}),
+             ("dedicated_small_large", {"kv_capacity_tokens": 5000, "delta_t": 0.011})]
+    for pol, over in cases:
+        cfg = abi.default_config(pol, m)
+        for k, v in over.items():
+            setattr(cfg, k, v)
+        got = run_engine(gpu, cfg, traces, ps)
+        for r, tr in enumerate(traces):
+            want = O.ora_run(cfg, tr, ps[r])
+            assert O.compare(got[r], want) == [], (pol, over, r)
