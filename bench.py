@@ -644,16 +644,24 @@ def main():
         # peak = the measured DMUL+DADD rate (profiles/fp64_peak.json).
         dims = agent_for(m)[0]
         macs = sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
-        flop = sum(2.0 * macs * float(st["ticks"].sum()) for _, st, _ in rl_cells)
+        dense = sum(2.0 * macs * float(st["ticks"].sum()) for _, st, _ in rl_cells)
+        # executed: the kernels count the multiply-adds their forwards issued
+        # (rs_replay_stats.qnet_macs: exact-zero inputs skipped, a repeated
+        # state's action reused without a forward)
+        flop = sum(2.0 * float(st["qnet_macs"].sum()) for _, st, _ in rl_cells)
+        dec = sum(float(st["ticks"].sum()) for _, st, _ in rl_cells)
         sec = sum(ms for _, _, ms in rl_cells) / 1e3
         fp = ROOT / "profiles" / "fp64_peak.json"
         fpeak = json.loads(fp.read_text())["fp64_tflops_mul_add"] if fp.exists() else None
         line["roofline_fp64_qnet"] = {
             "bound": "fp64", "achieved": flop / sec / 1e12, "peak": fpeak, "unit": "TFLOP/s",
             "frac": (flop / sec / 1e12 / fpeak) if fpeak else None,
-            "flop_per_decision": 2 * macs, "dims": dims,
-            "note": "dense-equivalent FLOPs of the Q-net forward over the RL cells' kernel time "
-                    "(the whole fused tick, not the forward alone; zero inputs are skipped)",
+            "flop_per_decision_executed": flop / max(1.0, dec),
+            "flop_per_decision_dense": 2 * macs, "dims": dims,
+            "dense_equivalent_tflops": dense / sec / 1e12,
+            "note": "EXECUTED FLOPs of the Q-net forwards (DMUL + DADD issued: exact-zero "
+                    "inputs skipped, repeated states memoised) over the RL cells' kernel time "
+                    "(the whole fused tick, not the forward alone)",
             "peak_source": "measured DMUL+DADD (profiles/fp64_peak.json, tools/fp64_peak.cu)"}
     if len(cells) > 1:
         line["per_policy"] = {c["policy"]: {"decisions": int(st["ticks"].sum()),

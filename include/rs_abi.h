@@ -267,7 +267,10 @@ typedef struct rs_replay_stats {
   int32_t percentiles_valid;
   int32_t _pad0;
   int64_t injected;             /* requests that reached the router queue */
-  int32_t _pad[4];
+  int64_t qnet_macs;            /* RL: multiply-adds the Q-network forwards executed
+                                   (exact-zero inputs skipped, a repeated state's
+                                   action reused); 0 for the heuristics */
+  int32_t _pad[2];
 } rs_replay_stats;
 
 /* ---- identity / device ------------------------------------------------ */

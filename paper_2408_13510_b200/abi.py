@@ -172,7 +172,8 @@ class ReplayStats(C.Structure):
         ("percentiles_valid", C.c_int32),
         ("_pad0", C.c_int32),
         ("injected", C.c_int64),
-        ("_pad", C.c_int32 * 4),
+        ("qnet_macs", C.c_int64),
+        ("_pad", C.c_int32 * 2),
     ]
 
 
@@ -237,7 +238,8 @@ STATS_DTYPE = np.dtype(
                                  "e2e_p99", "ttft_p50", "ttft_p90", "ttft_p99", "tbt_p50",
                                  "tbt_p90", "tbt_p99")]
     + [("status", np.int32), ("error_instance", np.int32), ("percentiles_valid", np.int32),
-       ("_pad0", np.int32), ("injected", np.int64), ("_pad", np.int32, (4,))])
+       ("_pad0", np.int32), ("injected", np.int64), ("qnet_macs", np.int64),
+       ("_pad", np.int32, (2,))])
 assert STATS_DTYPE.itemsize == 256
 
 

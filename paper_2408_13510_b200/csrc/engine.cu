@@ -9,7 +9,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -284,6 +286,41 @@ WsLayout ws_layout(int64_t total_requests, int64_t num_replays, size_t rl_params
   return w;
 }
 
+// Per-device caches of the planner's kernel queries: the dynamic shared-memory
+// opt-in of a kernel only ever rises, and the occupancy of (kernel, block,
+// bytes) is fixed, so repeated calls do not repeat the driver round trips.
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, int> g_smem_set;
+std::map<std::tuple<int, const void*, int, size_t>, int> g_occ;
+
+cudaError_t set_smem(const void* k, int bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  int& cur = g_smem_set[{dev, k}];
+  if (cur >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+
+cudaError_t occ_blocks(int* out, const void* k, int threads, size_t bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(g_attr_mu);
+  const auto key = std::make_tuple(dev, k, threads, bytes);
+  const auto it = g_occ.find(key);
+  if (it != g_occ.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, k, threads, bytes);
+  if (e == cudaSuccess) g_occ[key] = *out;
+  return e;
+}
+
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
@@ -292,11 +329,11 @@ int env_int(const char* name, int dflt) {
 template <typename K>
 rs_status launch_kernel(K kern, const rs::KParams& kp, int wpb, int groups_per_warp,
                         int block_smem, int num_replays, cudaStream_t st) {
-  RS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, block_smem));
+  RS_CUDA(set_smem((const void*)kern, block_smem));
   int dev = 0, sms = 0, per_sm = 0;
   RS_CUDA(cudaGetDevice(&dev));
   RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  RS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, wpb * rs::kWarp, block_smem));
+  RS_CUDA(occ_blocks(&per_sm, (const void*)kern, wpb * rs::kWarp, block_smem));
   if (per_sm < 1) return fail(RS_ERR_UNSUPPORTED, "replay kernel does not fit on an SM");
   const int per_block = wpb * groups_per_warp;
   const int want = (num_replays + per_block - 1) / per_block;
@@ -817,13 +854,13 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
       const long long bytes = L.weights_bytes + (long long)wpb * gpw * L.group_bytes;
       if (bytes > smem_optin) continue;
       KernelFn k = wpb > 8 ? wide : narrow;
-      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      if (set_smem((const void*)k, (int)bytes) !=
           cudaSuccess) {
         cudaGetLastError();
         continue;
       }
       int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, wpb * rs::kWarp,
+      if (occ_blocks(&per_sm, (const void*)k, wpb * rs::kWarp,
                                                         (size_t)bytes) != cudaSuccess) {
         cudaGetLastError();
         continue;
@@ -864,9 +901,8 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
                                                                       pl.width, 2, tail);
           int lat_blocks = 0;
           if (lat &&
-              cudaFuncSetAttribute(lat, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   pl.block_smem) == cudaSuccess &&
-              cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lat_blocks, lat, wpb * rs::kWarp,
+              set_smem((const void*)lat, pl.block_smem) == cudaSuccess &&
+              occ_blocks(&lat_blocks, (const void*)lat, wpb * rs::kWarp,
                                                             (size_t)pl.block_smem) == cudaSuccess &&
               lat_blocks >= 1)
             pl.kern = lat;
@@ -884,9 +920,9 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     KernelFn lat = kernel_for(cfg->policy, fast, groups, pl.width, 2, tail);
     int lat_blocks = 0;
     if (lat &&
-        cudaFuncSetAttribute(lat, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.block_smem) ==
+        set_smem((const void*)lat, pl.block_smem) ==
             cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&lat_blocks, lat, pl.wpb * rs::kWarp,
+        occ_blocks(&lat_blocks, (const void*)lat, pl.wpb * rs::kWarp,
                                                       (size_t)pl.block_smem) == cudaSuccess &&
         lat_blocks >= 1)
       pl.kern = lat;
@@ -899,9 +935,9 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     KernelFn lso = kernel_for(cfg->policy, fast, groups, pl.width, 3, tail);
     int blocks = 0;
     if (lat && lso && pl.kern == lat &&
-        cudaFuncSetAttribute(lso, cudaFuncAttributeMaxDynamicSharedMemorySize, pl.block_smem) ==
+        set_smem((const void*)lso, pl.block_smem) ==
             cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, lso, pl.wpb * rs::kWarp,
+        occ_blocks(&blocks, (const void*)lso, pl.wpb * rs::kWarp,
                                                       (size_t)pl.block_smem) == cudaSuccess &&
         blocks >= 1) {
       pl.kern = lso;
@@ -959,9 +995,9 @@ rs_status rs_internal_replay_batch(const rs_batch_cfg* cfg, const rs_trace_soa* 
     for (ppb = want; ppb >= 1; --ppb) {
       const int bytes = ppb * L.group_bytes;
       if (bytes > smem_optin) continue;
-      if (cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) !=
+      if (set_smem((const void*)pk, bytes) !=
               cudaSuccess ||
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pair_blocks, pk, 64 * ppb,
+          occ_blocks(&pair_blocks, (const void*)pk, 64 * ppb,
                                                         (size_t)bytes) != cudaSuccess) {
         cudaGetLastError();
         pair_blocks = 0;

@@ -35,7 +35,8 @@ struct MlpView {
 // `q_out` (may be nullptr) and returns argmax_action (dqn.hpp:82-90).
 template <int W>
 __device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double* h0,
-                                       double* h1, double* q_out, const Lanes<W>& L) {
+                                       double* h1, double* q_out, const Lanes<W>& L,
+                                       long long* macs = nullptr) {
   const int l = L.l;
   const double* cur = x;
   unsigned long long best_key = 0;
@@ -47,6 +48,7 @@ __device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double
     const double* B = M.w + M.boff[layer];
     const bool last = (layer + 1 == M.layers);
     double* dst = (layer & 1) ? h1 : h0;
+    int nz = 0;  // nonzero inputs (uniform)
     for (int ob = 0; ob < no; ob += 2 * W) {
       const int o0 = ob + l, o1 = ob + W + l;
       const bool v0 = o0 < no, v1 = o1 < no;
@@ -56,6 +58,7 @@ __device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double
       for (int i = 0; i < ni; ++i) {
         const double xi = cur[i];
         if (xi != 0.0) {
+          nz += ob == 0;
           const double* row = WT + (size_t)i * no;
           const double w0 = v0 ? row[o0] : 0.0;
           const double w1 = v1 ? row[o1] : 0.0;
@@ -84,6 +87,7 @@ __device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double
     }
     L.sync();
     cur = dst;
+    if (macs) *macs += (long long)nz * no;
   }
   const unsigned long long gmax = L.max_u64(have ? best_key : 0ull);
   const int cand = (have && best_key == gmax) ? best_idx : 0x7fffffff;
@@ -114,7 +118,7 @@ constexpr int kMlpSmemMaxWidth = kMlpMaskWords * kWarp;
 template <int W>
 __device__ inline int mlp_forward_list(const int* dims, const int* woff, const int* boff,
                                        int layers, int xd, int h0d, int h1d, int lvd,
-                                       const Lanes<W>& L) {
+                                       const Lanes<W>& L, long long& macs) {
   (void)h1d;  // h0 | h1 (contiguous, 2 x maxw doubles) hold the second record list
   const int l = L.l;
   const unsigned lt = L.lt();
@@ -212,6 +216,7 @@ __device__ inline int mlp_forward_list(const int* dims, const int* woff, const i
       }
     }
     L.sync();
+    macs += (long long)nnz * no;
     nnz = nout;
   }
   const unsigned long long gmax = L.max_u64(have ? best_key : 0ull);

@@ -225,6 +225,7 @@ __device__ __forceinline__ FastRun run_replay_pair(const KParams& P, int gw, cha
   R.rr_next = R.dsl_next = 0;
   R.mc_next = 0.0;
   R.hash = 0xcbf29ce484222325ull;
+  R.qmacs = 0;
   R.infeasible = R.routed = R.sum_q = R.sum_w = 0;
   R.status = RS_REPLAY_FINISHED;
   R.err_inst = -1;

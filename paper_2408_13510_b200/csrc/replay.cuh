@@ -63,6 +63,8 @@ struct Replay {  // per-replay registers (uniform across the warp)
   int hr_q, hr_prompt, hr_true, hr_bucket;
   int pred_pos;  // fused predictor: next unread mt19937_64 output (312 = regenerate)
   int resident_seen;  // streamed inputs: watermark seen
+  int rl_prev;  // fast kernel, RL: greedy action of the state held in x (-1: none)
+  long long qmacs;  // RL: Q-network multiply-adds executed
 };
 
 __device__ __forceinline__ Grp make_grp(const KParams& P, char* base) {

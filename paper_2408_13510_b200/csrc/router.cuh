@@ -344,7 +344,7 @@ __device__ inline int decide(const KParams& P, const Grp& G, const MlpView& M, R
     }
     double* h0 = x + M.dims[0];
     double* h1 = h0 + P.rl_maxw;
-    return mlp_forward_warp(M, x, h0, h1, nullptr, l);
+    return mlp_forward_warp(M, x, h0, h1, nullptr, warp_lanes(l), &R.qmacs);
   } else {
     // argmin policies: decode_balancer / jsq / min_min / workload_aware
     if (!has_head) return m;
@@ -405,6 +405,7 @@ __device__ inline void write_replay_stats(const KParams& P, const Replay& R, int
     s.status = R.status;
     s.error_instance = R.err_inst;
     s.injected = R.cursor;
+    s.qnet_macs = R.qmacs;
   }
   L.sync();
 }
@@ -567,6 +568,7 @@ __device__ void run_replay(const KParams& P, const Grp& G, const MlpView& M, int
   R.rr_next = R.dsl_next = 0;
   R.mc_next = 0.0;
   R.hash = 0xcbf29ce484222325ull;
+  R.qmacs = 0;
   R.infeasible = R.routed = R.sum_q = R.sum_w = 0;
   R.status = RS_REPLAY_FINISHED;
   R.err_inst = -1;

@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kStatsThreads, 3) stats_kernel(const __grid_co
       s.last_completion_s = lc;
       s.makespan_s = __dsub_rn(lc, fa);
       s._pad0 = 0;
-      for (int k = 0; k < 4; ++k) s._pad[k] = 0;
+      for (int k = 0; k < 2; ++k) s._pad[k] = 0;
     }
     __syncthreads();
   }

@@ -340,3 +340,28 @@ def test_no_head_windows_match_oracle(gpu, kernel_path, m, monkeypatch):
         for r, tr in enumerate(traces):
             want = O.ora_run(cfg, tr, ps[r])
             assert O.compare(got[r], want) == [], (pol, over, r)
+
+
+def test_qnet_mac_counter(gpu, kernel_path):
+    """rs_replay_stats.qnet_macs: the Q-network multiply-adds the replay's
+    forwards executed — positive for the RL router, at most the dense count
+    per decision (zero inputs skipped, repeated states memoised), 0 for the
+    heuristics; the decisions themselves stay bit-exact."""
+    m = 4
+    tb = engine.build_workload(range(90, 93), 500, 25.0)
+    traces = [O.Trace(tb.arrival[tb.replay(r)], tb.prompt[tb.replay(r)],
+                      tb.decode[tb.replay(r)], tb.task[tb.replay(r)]) for r in range(3)]
+    ps = [abi.mix_seed(s, 0x9DED) for s in range(90, 93)]
+    sd = abi.state_dimension(m)
+    dims = [sd, 64, 64, m + 1]
+    params = engine.mlp_random_init(dims, 42)
+    cfg = abi.default_config("rl", m)
+    keep = abi.set_rl(cfg, dims, params)  # noqa: F841 (keeps the weights alive)
+    dense = sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
+    got = run_engine(gpu, cfg, traces, ps)
+    for r, tr in enumerate(traces):
+        assert O.compare(got[r], O.ora_run(cfg, tr, ps[r])) == []
+        st = got[r].stats[0]
+        assert 0 < int(st["qnet_macs"]) < dense * int(st["ticks"])
+    got = run_engine(gpu, abi.default_config("jsq", m), traces, ps)
+    assert all(int(g.stats[0]["qnet_macs"]) == 0 for g in got)
