@@ -353,7 +353,7 @@ __device__ __forceinline__ unsigned long long mt_tw(unsigned long long a, unsign
 }
 
 template <int W>
-__device__ inline void mt_twist(unsigned long long* s, const Lanes<W>& L) {
+__device__ __forceinline__ void mt_twist_impl(unsigned long long* s, const Lanes<W>& L) {
   const int l = L.l;
   if (W == kWarp) {
     unsigned long long nv[5];
@@ -403,6 +403,13 @@ __device__ inline void mt_twist(unsigned long long* s, const Lanes<W>& L) {
   L.sync();
 }
 
+// Out of line: a twist runs once per 312 draws, and inlined at every call
+// site its unrolled phases would crowd the tick loop out of the instruction
+// cache (the RL replay kernel was 37k instructions).
+template <int W>
+__device__ __noinline__ void mt_twist(unsigned long long* s, const Lanes<W> L) {
+  mt_twist_impl(s, L);
+}
 __device__ inline void mt_twist_warp(unsigned long long* s, int l) { mt_twist(s, warp_lanes(l)); }
 
 __device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
@@ -415,7 +422,7 @@ __device__ __forceinline__ unsigned long long mt_temper(unsigned long long y) {
 
 // Seeding (std::mt19937_64 constructor); serial recurrence, group lane 0.
 template <int W>
-__device__ inline void mt_seed(unsigned long long* s, unsigned long long seed, const Lanes<W>& L) {
+__device__ __noinline__ void mt_seed(unsigned long long* s, unsigned long long seed, const Lanes<W> L) {
   if (L.l == 0) {
     s[0] = seed;
     for (int i = 1; i < 312; ++i)

@@ -303,13 +303,16 @@ __device__ __forceinline__ int decide_fast(const KParams& P, int gw, const MlpVi
 // predict_simulated predictor.hpp:98-110: one draw, a second for a miss in a
 // middle bucket).  The stream is policy independent, so drawing a window
 // ahead of injection is equivalent.  Written to the predicted-bucket output.
+// Out of line (once per 32 arrivals): inlined, the draw loop and its bucket
+// searches sat in the tick loop's instruction footprint.  Returns the
+// stream position after the window.
 template <int W>
-__device__ __forceinline__ void predict_window(const KParams& P, Replay& R, unsigned long long* pst,
-                                      const Lanes<W>& L) {
+__device__ __noinline__ int predict_window_cold(const KParams& P, int a_base, int n, long long off,
+                                                int pos, unsigned long long* pst, const Lanes<W> L) {
   const int l = L.l;
-  const int j = R.a_base + l;
-  const bool v = j < R.n;
-  const long long g = R.off + j;
+  const int j = a_base + l;
+  const bool v = j < n;
+  const long long g = off + j;
   int pred = 0;
   if (P.predictor_mode == RS_PREDICTOR_GIVEN) {
     if (v) pred = P.given_bucket[g];
@@ -323,17 +326,17 @@ __device__ __forceinline__ void predict_window(const KParams& P, Replay& R, unsi
       tb = bucket_of(P.pred_edges, nb, P.decode[g]);
       acc = P.accuracy[P.task[g]];
     }
-    const int cnt = min(W, R.n - R.a_base);
+    const int cnt = min(W, n - a_base);
     for (int k = 0; k < cnt; ++k) {
       const int tbk = L.shfl(tb, k);
       const double ak = L.shfl(acc, k);
       int pk = 0;
       if (nb > 1) {
-        if (R.pred_pos == 312) {
+        if (pos == 312) {
           mt_twist(pst, L);  // outputs are tempered as they are drawn
-          R.pred_pos = 0;
+          pos = 0;
         }
-        const double u = u01(mt_temper(pst[R.pred_pos++]));
+        const double u = u01(mt_temper(pst[pos++]));
         if (u < ak) {
           pk = tbk;
         } else if (tbk == 0) {
@@ -341,11 +344,11 @@ __device__ __forceinline__ void predict_window(const KParams& P, Replay& R, unsi
         } else if (tbk == nb - 1) {
           pk = nb - 2;
         } else {
-          if (R.pred_pos == 312) {
+          if (pos == 312) {
             mt_twist(pst, L);
-            R.pred_pos = 0;
+            pos = 0;
           }
-          pk = u01(mt_temper(pst[R.pred_pos++])) < 0.5 ? tbk - 1 : tbk + 1;
+          pk = u01(mt_temper(pst[pos++])) < 0.5 ? tbk - 1 : tbk + 1;
         }
       }
       if (l == k) pred = pk;
@@ -353,6 +356,12 @@ __device__ __forceinline__ void predict_window(const KParams& P, Replay& R, unsi
   }
   if (v) P.o_pred[g] = (uint8_t)pred;
   L.sync();
+  return pos;
+}
+template <int W>
+__device__ __forceinline__ void predict_window(const KParams& P, Replay& R, unsigned long long* pst,
+                                              const Lanes<W>& L) {
+  R.pred_pos = predict_window_cold(P, R.a_base, R.n, R.off, R.pred_pos, pst, L);
 }
 
 template <int W>

@@ -34,9 +34,9 @@ struct MlpView {
 // warp.  h0/h1: shared scratch of max width.  Writes the final layer to
 // `q_out` (may be nullptr) and returns argmax_action (dqn.hpp:82-90).
 template <int W>
-__device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double* h0,
-                                       double* h1, double* q_out, const Lanes<W>& L,
-                                       long long* macs = nullptr) {
+__device__ __forceinline__ int mlp_forward_warp_impl(const MlpView& M, const double* x, double* h0,
+                                                     double* h1, double* q_out, const Lanes<W>& L,
+                                                     long long* macs) {
   const int l = L.l;
   const double* cur = x;
   unsigned long long best_key = 0;
@@ -94,9 +94,20 @@ __device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double
   return L.min(cand);
 }
 
+// Out of line in the replay kernels: they call it only for Q-networks too
+// big for the staged forward (and the general kernel once per tick); inlined,
+// it doubled the tick loop's instruction footprint.
+template <int W>
+__device__ __noinline__ int mlp_forward_warp(const MlpView M, const double* x, double* h0,
+                                             double* h1, double* q_out, const Lanes<W> L,
+                                             long long* macs = nullptr) {
+  return mlp_forward_warp_impl(M, x, h0, h1, q_out, L, macs);
+}
+
+// The batched forward kernel (rs_mlp_forward): inline.
 __device__ inline int mlp_forward_warp(const MlpView& M, const double* x, double* h0,
                                        double* h1, double* q_out, int l) {
-  return mlp_forward_warp(M, x, h0, h1, q_out, warp_lanes(l));
+  return mlp_forward_warp_impl(M, x, h0, h1, q_out, warp_lanes(l), nullptr);
 }
 
 extern __shared__ __align__(16) double rs_smd[];
