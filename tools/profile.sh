@@ -14,7 +14,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     python bench.py --config "$cfg" --steps 2 --warmup 3 --no-e2e --no-cpu-baseline "$@" \
     > gpurun_out/launches_${cfg}_${tag}.log 2>&1
 echo "launch list rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:replay_fast_kernel -s ${SKIP:-3} -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:"replay_(fast|pair)_kernel" -s ${SKIP:-3} -c 1 \
     -o gpurun_out/full_${cfg}_${tag} -f \
     python bench.py --config "$cfg" --steps 1 --warmup 3 --no-e2e --no-cpu-baseline "$@" \
     > gpurun_out/full_${cfg}_${tag}.log 2>&1
